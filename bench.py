@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: decoded coded Gbit/s of the B200 LDPC decoder (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2]): DVB-S2-shaped
+irregular rate-1/2 code, n = 64800, E = 226,800, batch 1024 codewords per
+GPU, fixed 10 iterations (early stop off, fixed work), all-zero codeword over
+BPSK/AWGN at Eb/N0 = 2 dB (synthetic, seeded).  One step = one decode of the
+batch + the error-count reduction (NCCL allreduce across ranks when N > 1).
+
+  python bench.py [--gpus N --steps K --warmup W]           # our arm
+  python bench.py --impl reference [...]                     # reference CPU arm
+  torchrun --nproc-per-node N bench.py --gpus N ...          # N > 1 (weak scaling)
+
+Prints ONE JSON line on rank 0.  ``value`` is device-timed (CUDA events, max
+over ranks) with the priors already resident in HBM; ``e2e`` is the same
+metric through the public host API (ParallelDecoder.decode_priors: pinned host
+priors -> device -> packed results back to host every step).  The per-step
+working set (2.4 GB per GPU) is far larger than the 126 MB L2, so no L2
+flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decoded coded Gbit/s at 10 iters (n=64800), 1/2/4/8 B200; % of HBM roofline"
+UNIT = "Gbit/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--iters", type=int, default=None)
+    ap.add_argument("--ebno", type=float, default=2.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def synthetic_priors(H, B, ebno_db, seed):
+    """All-zero codeword, BPSK 0 -> -1, AWGN (channel.py:1-8); priors by the reference's numpy expression."""
+    from paper_1609_01567_b200 import configs, priors_awgn_batch
+
+    s2 = configs.ebno_to_sigma2(ebno_db, configs.rate(H))
+    rng = np.random.default_rng(seed)
+    Y = -1.0 + np.sqrt(s2) * rng.standard_normal((B, H.n))
+    return priors_awgn_batch(Y, s2), s2
+
+
+def workload_desc(cfg, H, B, iters, ebno):
+    return {"workload": f"{cfg}: DVB-S2-shaped irregular LDPC n={H.n} m={H.m} E={H.total_edges} rate 1/2 "
+                        f"(var deg 8/3/2, check deg 7), batch {B} codewords per GPU, fixed {iters} iterations",
+            "code": cfg, "n": H.n, "edges": H.total_edges, "batch_per_gpu": B, "iterations": iters,
+            "early_stop": False, "ebno_db": ebno,
+            "l2": "no flush needed: per-step working set ~2.4 GB/GPU >> 126 MB L2"}
+
+
+# ---- CPU reference (oracle port of the reference decoder, test-infrastructure) ----
+
+def cpu_reference_rate(H, P, iters, seconds):
+    """Time the oracle (C restatement of serial.py) on host threads: (Gbit/s, cores, frames, secs)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from oracle import OracleTables  # noqa: E402  (checker / CPU baseline only)
+
+    O = OracleTables.from_matrix(H)
+    cores = os.cpu_count() or 1
+    t = time.perf_counter()
+    O.decode_batch(P[:1], iters, fixed_iterations=True, n_threads=1)
+    per_frame = time.perf_counter() - t
+    frames = int(max(cores, min(len(P), round(seconds * cores / max(per_frame, 1e-3)))))
+    frames = max(cores, (frames // cores) * cores)
+    idx = np.arange(frames) % len(P)
+    Ps = np.ascontiguousarray(P[idx])
+    t = time.perf_counter()
+    O.decode_batch(Ps, iters, fixed_iterations=True, n_threads=cores)
+    secs = time.perf_counter() - t
+    return frames * H.n / secs / 1e9, cores, frames, secs
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from paper_1609_01567_b200 import configs
+
+    cfg = args.config
+    C = configs.CONFIGS[cfg]
+    H = configs.code(C["code"])
+    B = args.batch or C["batch"]
+    iters = args.iters if args.iters is not None else C["max_iterations"]
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from oracle import OracleTables
+
+    O = OracleTables.from_matrix(H)
+    cores = os.cpu_count() or 1
+    P, _ = synthetic_priors(H, 2 * cores, args.ebno, seed=7)
+    times = []
+    for step in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        O.decode_batch(P, iters, fixed_iterations=True, n_threads=cores)
+        dt = time.perf_counter() - t
+        if step >= args.warmup:
+            times.append(dt)
+    secs = float(np.sum(times))
+    value = len(P) * H.n * args.steps / secs / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: all-zero codeword, BPSK/AWGN at %.1f dB, seeded numpy normals" % args.ebno,
+        "config": workload_desc(cfg, H, B, iters, args.ebno),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"each step {len(P)} frames of the workload's code (fixed {iters} iterations) "
+                                   f"decoded by the C restatement of the reference decoder (oracle/) on "
+                                   f"{cores} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- clocks sampler ---------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.device_index = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device_index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 5 + i and s[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_traffic(kernel_class):
+    """dram bytes per launch from the committed `ncu --set full` summary (profiles/), or None."""
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    if not f.exists():
+        return None
+    try:
+        d = json.loads(f.read_text())
+        return d.get(kernel_class, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---- our arm ----------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_01567_b200 import CodeTables, ParallelDecoder, _native, configs
+
+    rank, local_rank, world = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    dev = torch.device(f"cuda:{local_rank}")
+    torch.cuda.set_device(dev)
+    cfg = args.config
+    C = configs.CONFIGS[cfg]
+    H = configs.code(C["code"])
+    B = args.batch or C["batch"]
+    iters = args.iters if args.iters is not None else C["max_iterations"]
+    T = CodeTables.from_matrix(H)
+    dec = ParallelDecoder(T, max_batch=B)
+    P_host, _ = synthetic_priors(H, B, args.ebno, seed=1000 + rank)
+    P_pin = torch.from_numpy(P_host).pin_memory()
+    P_dev = P_pin.to(dev, non_blocking=True)
+    ws = dec.workspace(B)
+    outs = dec.alloc_outputs(B, dev)
+    counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(profile=None):
+        dec.decode_device(P_dev, iters, early_stop=False, workspace=ws, outputs=outs, profile=profile)
+        dec.count_errors(outs, counts)
+        if world > 1:
+            dist.all_reduce(counts)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, barrier + synchronize on both sides, CUDA events, max over ranks
+    L = _native.load_library()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.ldpc_kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = L.ldpc_kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * B * H.n / (ms_step / 1e3) / 1e9
+
+    # per-kernel-class event timing over K profiled steps (same stream, same work)
+    prof = _native.Profile()
+    for _ in range(args.steps):
+        step(profile=prof)
+    torch.cuda.synchronize()
+    pd = prof.as_dict()
+    dom = max(("check", "variable"), key=lambda k: pd[k]["ms"])
+    per_launch_bytes = pd[dom]["bytes"] / max(pd[dom]["launches"], 1)
+    per_launch_ms = pd[dom]["ms"] / max(pd[dom]["launches"], 1)
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    step_ms_prof = sum(v["ms"] for v in pd.values()) / args.steps
+    algo_bytes_step = sum(v["bytes"] for v in pd.values()) / args.steps
+
+    # e2e through the public host API: pinned priors in, packed results out, every step
+    e2e = None
+    if not args.no_e2e:
+        from paper_1609_01567_b200.decoder import BatchResult
+
+        n, m = H.n, H.m
+        pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory().numpy()  # noqa: E731
+        res = BatchResult(pin((B, (n + 31) // 32), torch.int32).view(np.uint32), pin((B,), torch.uint8),
+                          pin((B,), torch.int32), pin((B, (m + 31) // 32), torch.int32).view(np.uint32), n, m)
+        Pn = P_pin.numpy()
+        for _ in range(max(1, args.warmup)):
+            dec.decode_priors(Pn, iters, early_stop=False, out=res)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            dec.decode_priors(Pn, iters, early_stop=False, out=res)
+        el = time.perf_counter() - t0
+        tt = torch.tensor([el], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+        e2e = {"value": world * B * n * args.steps / el / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(Pn.nbytes),
+               "d2h_bytes_per_step": int(res.est_bits.nbytes + res.success.nbytes + res.iterations.nbytes
+                                         + res.syn_bits.nbytes),
+               "ms_per_step": 1e3 * el / args.steps,
+               "path": "ParallelDecoder.decode_priors (ldpc_decoder_decode_host: pinned H2D, decode, D2H, "
+                       "pipelined over 2 streams)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, frames, secs = cpu_reference_rate(H, P_host, iters, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{frames} frames of the workload (fixed {iters} iterations) in {secs:.1f} s by the C "
+                         f"restatement of the reference decoder (oracle/) on {cores} host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: all-zero codeword, BPSK/AWGN at %.1f dB, seeded numpy normals; priors by the "
+                    "reference's numpy expression" % args.ebno,
+            "config": dict(workload_desc(cfg, H, B, iters, args.ebno),
+                           parallelism=f"dp{world}: independent codeword shards, NCCL allreduce of error counts"),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": load_traffic(dom), "kernel": dom,
+                         "algorithmic_bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_ms,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6.65 TB/s",
+                         "step_algorithmic_GBps": algo_bytes_step / (step_ms_prof / 1e3) / 1e9,
+                         "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in pd.items()}},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "counts": {"bit_errors": int(counts[0]), "failures": int(counts[1]), "iterations": int(counts[2]),
+                       "frames": int(counts[3])},
+        }
+        print(json.dumps(line), flush=True)
+    dec.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,436 @@
+// decode.cu -- G5: batched decode driver, single-phase entry points, and the
+// host-buffer decoder (the C-ABI the Python ParallelDecoder mirror calls).
+//
+// Phase order (serial.py:150-178 / engine.py:311-347, paper Algorithm 2):
+//     r = C(p[v]);  c = Est(p, r);  z = Syn(c);  stop if z == 0      (round 0)
+//     for t in 1..I:  q = V(p, r);  r = C(q);  c = Est(p, r);  z = Syn(c);  stop if z == 0
+// Kernel sequence used here (Est(t-1) is fused into V(t) because both read the
+// same r and p; the final estimate is a V pass without the q write):
+//     C0   VE1 [S0 U0]  C1   VE2 [S1 U1]  C2  ...  VE_I [S_{I-1} U_{I-1}]  C_I   E_I  S_I [U_I]
+// where S = syndrome + OR-reduced unsatisfied flags and U = early-stop update
+// ([..] only in early-stop mode).  A codeword that stops at round t keeps its
+// round-t estimate (frozen bits) and iteration count; its later message
+// updates are wasted but harmless, and warps whose 32*V codewords have all
+// stopped skip their work.  All control stays on the device: no host sync
+// between rounds.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace ldpc {
+
+namespace {
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+}  // namespace
+
+size_t workspace_bytes(const ldpc_graph *g, int32_t B) {
+    const size_t Bp = (size_t)padded_batch(B), NW = Bp / 32;
+    size_t b = 0;
+    b += align256(sizeof(double) * (size_t)g->E * Bp);
+    b += align256(sizeof(double) * (size_t)g->n * Bp);
+    b += align256(sizeof(uint32_t) * (size_t)g->n * NW);
+    b += align256(sizeof(uint32_t) * (size_t)g->m * NW);
+    b += align256(sizeof(uint32_t) * NW) * 2;
+    b += align256(sizeof(int32_t) * Bp);
+    return b;
+}
+
+int carve_workspace(const ldpc_graph *g, int32_t B, void *ws, size_t bytes, Workspace *w) {
+    LDPC_ARG_CHECK(B >= 1, "batch must be at least 1");
+    const size_t need = workspace_bytes(g, B);
+    LDPC_ARG_CHECK(ws != nullptr && bytes >= need, "workspace too small: %zu < %zu bytes", bytes, need);
+    LDPC_ARG_CHECK(((uintptr_t)ws & 255) == 0, "workspace must be 256-byte aligned");
+    w->B = B;
+    w->Bp = padded_batch(B);
+    w->NW = w->Bp / 32;
+    char *p = (char *)ws;
+    auto take = [&](size_t sz) {
+        char *r = p;
+        p += align256(sz);
+        return r;
+    };
+    w->msg = (double *)take(sizeof(double) * (size_t)g->E * w->Bp);
+    w->P = (double *)take(sizeof(double) * (size_t)g->n * w->Bp);
+    w->chat = (uint32_t *)take(sizeof(uint32_t) * (size_t)g->n * w->NW);
+    w->zb = (uint32_t *)take(sizeof(uint32_t) * (size_t)g->m * w->NW);
+    w->done = (uint32_t *)take(sizeof(uint32_t) * w->NW);
+    w->unsat = (uint32_t *)take(sizeof(uint32_t) * w->NW);
+    w->iters = (int32_t *)take(sizeof(int32_t) * w->Bp);
+    return LDPC_OK;
+}
+
+namespace {
+
+// ---- per-kernel-class event timing ------------------------------------------
+struct Prof {
+    ldpc_profile *out = nullptr;
+    cudaStream_t s = nullptr;
+    struct Mark {
+        int cls;
+        cudaEvent_t a, b;
+        int64_t bytes;
+    };
+    std::vector<Mark> marks;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    cudaEvent_t get() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    cudaEvent_t begin() {
+        if (!out) return nullptr;
+        cudaEvent_t e = get();
+        cudaEventRecord(e, s);
+        return e;
+    }
+    void end(int cls, cudaEvent_t a, int64_t bytes) {
+        if (!out) return;
+        cudaEvent_t e = get();
+        cudaEventRecord(e, s);
+        marks.push_back(Mark{cls, a, e, bytes});
+    }
+    int flush() {
+        if (!out || marks.empty()) return LDPC_OK;
+        LDPC_CUDA_TRY(cudaEventSynchronize(marks.back().b));
+        for (auto &m : marks) {
+            float ms = 0.f;
+            LDPC_CUDA_TRY(cudaEventElapsedTime(&ms, m.a, m.b));
+            out->ms[m.cls] += ms;
+            out->launches[m.cls] += 1;
+            out->bytes[m.cls] += m.bytes;
+        }
+        marks.clear();
+        used = 0;
+        return LDPC_OK;
+    }
+    ~Prof() {
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+#define RUN(cls, bytes, call)                     \
+    do {                                          \
+        cudaEvent_t _a = prof.begin();            \
+        int _rc = (call);                         \
+        if (_rc != LDPC_OK) return _rc;           \
+        prof.end((cls), _a, (int64_t)(bytes));    \
+    } while (0)
+
+NodeLaunch check_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
+    return NodeLaunch{g->chk_off, g->chk_var, g->chk_order, 0, 0, w.msg, w.P, nullptr, done, w.Bp, w.NW};
+}
+
+NodeLaunch var_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
+    return NodeLaunch{g->var_off, g->var_pos, g->var_order, 0, 0, w.msg, w.P, w.chat, done, w.Bp, w.NW};
+}
+
+int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const uint32_t *done, cudaStream_t s) {
+    NodeLaunch a = check_args(g, w, done);
+    int wide_begin = -1, wide_end = 0, wide_max = 0;
+    for (const Bucket &b : g->chk_buckets) {
+        if (b.deg <= kMaxRegDegree) {
+            a.node_begin = b.node_begin;
+            a.node_count = b.node_count;
+            int rc = launch_check_bucket(a, b.deg, from_prior, s);
+            if (rc) return rc;
+        } else {
+            if (wide_begin < 0) wide_begin = b.node_begin;
+            wide_end = b.node_begin + b.node_count;
+            wide_max = std::max(wide_max, b.deg);
+        }
+    }
+    if (wide_begin >= 0) {
+        a.node_begin = wide_begin;
+        a.node_count = wide_end - wide_begin;
+        return launch_check_wide(a, wide_max, from_prior, s);
+    }
+    return LDPC_OK;
+}
+
+int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint32_t *done, cudaStream_t s) {
+    NodeLaunch a = var_args(g, w, done);
+    int wide_begin = -1, wide_end = 0, wide_max = 0;
+    for (const Bucket &b : g->var_buckets) {
+        if (b.deg <= kMaxRegDegree) {
+            a.node_begin = b.node_begin;
+            a.node_count = b.node_count;
+            int rc = launch_var_bucket(a, b.deg, write_q, s);
+            if (rc) return rc;
+        } else {
+            if (wide_begin < 0) wide_begin = b.node_begin;
+            wide_end = b.node_begin + b.node_count;
+            wide_max = std::max(wide_max, b.deg);
+        }
+    }
+    if (wide_begin >= 0) {
+        a.node_begin = wide_begin;
+        a.node_count = wide_end - wide_begin;
+        return launch_var_wide(a, wide_max, write_q, s);
+    }
+    return LDPC_OK;
+}
+
+// done bits of padded codewords (>= B) are set from the start in early-stop mode
+int init_flags(const Workspace &w, bool early, cudaStream_t s) {
+    LDPC_CUDA_TRY(cudaMemsetAsync(w.unsat, 0, sizeof(uint32_t) * w.NW, s));
+    LDPC_CUDA_TRY(cudaMemsetAsync(w.done, 0, sizeof(uint32_t) * w.NW, s));
+    if (early) {
+        LDPC_CUDA_TRY(cudaMemsetAsync(w.iters, 0, sizeof(int32_t) * w.Bp, s));
+        const int full = w.B / 32;
+        if (w.B % 32) {
+            int rc = launch_fill_u32(w.done + full, ~((1u << (w.B % 32)) - 1u), 1, s);
+            if (rc) return rc;
+        }
+        const int first_pad_word = (w.B + 31) / 32;
+        int rc = launch_fill_u32(w.done + first_pad_word, 0xffffffffu, (size_t)(w.NW - first_pad_word), s);
+        if (rc) return rc;
+    }
+    return LDPC_OK;
+}
+
+}  // namespace
+
+// The decode proper on a carved workspace whose P is filled.
+int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s, Prof &prof) {
+    const int64_t B = w.B, E = g->E, n = g->n, m = g->m;
+    const int64_t c_bytes = 16 * E * B;                   // read q (or p-gather) + write r
+    const int64_t ve_bytes = (16 * E + 8 * n + n / 8) * B; // read r, p; write q, c_hat bits
+    const int64_t e_bytes = (8 * E + 8 * n + n / 8) * B;   // read r, p; write c_hat bits
+    const int64_t s_bytes = (n / 8) * B;                  // read c_hat bits
+    int rc = init_flags(w, early, s);
+    if (rc) return rc;
+    const uint32_t *done = early ? w.done : nullptr;
+    RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, true, nullptr, s));
+    for (int32_t t = 1; t <= max_iter; t++) {
+        RUN(LDPC_KCLASS_VARIABLE, ve_bytes, var_phase(g, w, true, done, s));
+        if (early) {
+            RUN(LDPC_KCLASS_SYNDROME, s_bytes, launch_syndrome(g, w, false, true, s));
+            RUN(LDPC_KCLASS_SYNDROME, 0, launch_update_done(w, t - 1, false, s));
+        }
+        RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, false, done, s));
+    }
+    RUN(LDPC_KCLASS_ESTIMATE, e_bytes, var_phase(g, w, false, done, s));
+    RUN(LDPC_KCLASS_SYNDROME, s_bytes + (m / 8) * B, launch_syndrome(g, w, true, early, s));
+    if (early) RUN(LDPC_KCLASS_SYNDROME, 0, launch_update_done(w, max_iter, true, s));
+    (void)m;
+    return LDPC_OK;
+}
+
+}  // namespace ldpc
+
+using namespace ldpc;
+
+extern "C" size_t ldpc_workspace_bytes(const ldpc_graph *g, int32_t B) {
+    if (!g || B < 1) return 0;
+    return workspace_bytes(g, B);
+}
+
+extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, int32_t max_iterations,
+                           uint32_t flags, uint32_t *est_bits_dev, uint8_t *success_dev, int32_t *iters_dev,
+                           uint32_t *syn_bits_dev, void *workspace_dev, size_t workspace_bytes_, void *stream,
+                           ldpc_profile *prof_host) {
+    LDPC_ARG_CHECK(g != nullptr, "NULL graph");
+    LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
+    LDPC_ARG_CHECK(p_dev && est_bits_dev && success_dev && iters_dev, "NULL output/input pointer");
+    LDPC_ARG_CHECK(flags <= LDPC_FLAG_FIXED_ITERS, "unknown flags 0x%x", flags);
+    Workspace w;
+    int rc = carve_workspace(g, B, workspace_dev, workspace_bytes_, &w);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
+    Prof prof;
+    prof.out = prof_host;
+    prof.s = s;
+    const int64_t n = g->n, m = g->m;
+    RUN(LDPC_KCLASS_LAYOUT, 16 * n * B, launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s));
+    rc = run_decode(g, w, max_iterations, early, s, prof);
+    if (rc) return rc;
+    RUN(LDPC_KCLASS_LAYOUT, (n / 8) * 2 * B, launch_pack_rows(w.chat, g->n, w.NW, B, est_bits_dev, s));
+    if (syn_bits_dev) RUN(LDPC_KCLASS_LAYOUT, (m / 8) * 2 * B, launch_pack_rows(w.zb, g->m, w.NW, B, syn_bits_dev, s));
+    RUN(LDPC_KCLASS_LAYOUT, 0, launch_finalize(w, early, max_iterations, success_dev, iters_dev, s));
+    return prof.flush();
+}
+
+extern "C" int ldpc_count_errors(const ldpc_graph *g, const uint32_t *est_bits_dev, const uint8_t *success_dev,
+                                 const int32_t *iters_dev, int32_t B, int64_t *counts_dev, void *stream) {
+    LDPC_ARG_CHECK(g && est_bits_dev && success_dev && iters_dev && counts_dev, "NULL argument");
+    LDPC_ARG_CHECK(B >= 1, "batch must be at least 1");
+    return launch_count_errors(est_bits_dev, (g->n + 31) / 32, success_dev, iters_dev, B, counts_dev,
+                               (cudaStream_t)stream);
+}
+
+// ---- single phases -----------------------------------------------------------
+extern "C" int ldpc_phase_to_variable(const ldpc_graph *g, const double *q_dev, double *r_dev, int32_t B,
+                                      void *ws, size_t ws_bytes, void *stream) {
+    LDPC_ARG_CHECK(g && q_dev && r_dev, "NULL argument");
+    Workspace w;
+    int rc = carve_workspace(g, B, ws, ws_bytes, &w);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((rc = launch_canon_to_slots(g, q_dev, B, w.msg, w.Bp, s))) return rc;
+    if ((rc = check_phase(g, w, false, nullptr, s))) return rc;
+    return launch_slots_to_canon(g, w.msg, w.Bp, r_dev, B, s);
+}
+
+extern "C" int ldpc_phase_to_check(const ldpc_graph *g, const double *p_dev, const double *r_dev, double *q_dev,
+                                   int32_t B, void *ws, size_t ws_bytes, void *stream) {
+    LDPC_ARG_CHECK(g && p_dev && r_dev && q_dev, "NULL argument");
+    Workspace w;
+    int rc = carve_workspace(g, B, ws, ws_bytes, &w);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((rc = launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s))) return rc;
+    if ((rc = launch_canon_to_slots(g, r_dev, B, w.msg, w.Bp, s))) return rc;
+    if ((rc = var_phase(g, w, true, nullptr, s))) return rc;
+    return launch_slots_to_canon(g, w.msg, w.Bp, q_dev, B, s);
+}
+
+extern "C" int ldpc_phase_estimate(const ldpc_graph *g, const double *p_dev, const double *r_dev,
+                                   uint8_t *chat_dev, int32_t B, void *ws, size_t ws_bytes, void *stream) {
+    LDPC_ARG_CHECK(g && p_dev && r_dev && chat_dev, "NULL argument");
+    Workspace w;
+    int rc = carve_workspace(g, B, ws, ws_bytes, &w);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((rc = launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s))) return rc;
+    if ((rc = launch_canon_to_slots(g, r_dev, B, w.msg, w.Bp, s))) return rc;
+    if ((rc = var_phase(g, w, false, nullptr, s))) return rc;
+    return launch_bits_to_bytes(w.chat, g->n, w.NW, B, chat_dev, s);
+}
+
+extern "C" int ldpc_phase_syndrome(const ldpc_graph *g, const uint8_t *chat_dev, uint8_t *z_dev, int32_t B,
+                                   void *ws, size_t ws_bytes, void *stream) {
+    LDPC_ARG_CHECK(g && chat_dev && z_dev, "NULL argument");
+    Workspace w;
+    int rc = carve_workspace(g, B, ws, ws_bytes, &w);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((rc = launch_bytes_to_bits(chat_dev, B, g->n, w.chat, w.NW, s))) return rc;
+    LDPC_CUDA_TRY(cudaMemsetAsync(w.unsat, 0, sizeof(uint32_t) * w.NW, s));
+    if ((rc = launch_syndrome(g, w, true, false, s))) return rc;
+    return launch_bits_to_bytes(w.zb, g->m, w.NW, B, z_dev, s);
+}
+
+// ---- host-buffer decoder: pipelined H2D / decode / D2H over two streams -------
+struct ldpc_decoder {
+    const ldpc_graph *g = nullptr;
+    int32_t max_batch = 0, sub = 0;
+    cudaStream_t st[2] = {nullptr, nullptr};
+    void *ws[2] = {nullptr, nullptr};
+    size_t ws_bytes = 0;
+    double *p[2] = {nullptr, nullptr};
+    uint32_t *est[2] = {nullptr, nullptr};
+    uint32_t *syn[2] = {nullptr, nullptr};
+    uint8_t *succ[2] = {nullptr, nullptr};
+    int32_t *its[2] = {nullptr, nullptr};
+    bool poisoned = false;
+    std::mutex mu;
+};
+
+static void decoder_free(ldpc_decoder *d) {
+    if (!d) return;
+    for (int i = 0; i < 2; i++) {
+        if (d->st[i]) cudaStreamSynchronize(d->st[i]);
+        cudaFree(d->ws[i]);
+        cudaFree(d->p[i]);
+        cudaFree(d->est[i]);
+        cudaFree(d->syn[i]);
+        cudaFree(d->succ[i]);
+        cudaFree(d->its[i]);
+        if (d->st[i]) cudaStreamDestroy(d->st[i]);
+    }
+    delete d;
+}
+
+extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32_t sub_batch, ldpc_decoder **out) {
+    LDPC_ARG_CHECK(g && out, "NULL argument");
+    LDPC_ARG_CHECK(max_batch >= 1, "max_batch must be at least 1");
+    *out = nullptr;
+    ldpc_decoder *d = new ldpc_decoder();
+    d->g = g;
+    d->max_batch = max_batch;
+    d->sub = sub_batch > 0 ? std::min(sub_batch, max_batch) : std::min(max_batch, 256);
+    d->ws_bytes = workspace_bytes(g, d->sub);
+    const size_t RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32;
+    for (int i = 0; i < 2; i++) {
+        cudaError_t e = cudaStreamCreateWithFlags(&d->st[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMalloc(&d->ws[i], d->ws_bytes);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&d->p[i], sizeof(double) * (size_t)g->n * d->sub);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&d->est[i], sizeof(uint32_t) * RWn * d->sub);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&d->syn[i], sizeof(uint32_t) * RWm * d->sub);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&d->succ[i], d->sub);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&d->its[i], sizeof(int32_t) * d->sub);
+        if (e != cudaSuccess) {
+            set_error("decoder allocation: %s", cudaGetErrorString(e));
+            decoder_free(d);
+            return e == cudaErrorMemoryAllocation ? LDPC_ENOMEM : LDPC_ECUDA;
+        }
+    }
+    *out = d;
+    return LDPC_OK;
+}
+
+extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, int32_t B, int32_t max_iterations,
+                                        uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
+                                        int32_t *iters_host, uint32_t *syn_bits_host) {
+    if (d == nullptr) {
+        set_error("decoder is closed");
+        return LDPC_ECLOSED;
+    }
+    std::lock_guard<std::mutex> lock(d->mu);
+    if (d->poisoned) {
+        set_error("decoder is closed after a device fault");
+        return LDPC_ECLOSED;
+    }
+    LDPC_ARG_CHECK(p_host && est_bits_host && success_host && iters_host, "NULL argument");
+    LDPC_ARG_CHECK(B >= 1 && B <= d->max_batch, "batch %d outside 1..%d", B, d->max_batch);
+    LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
+    const ldpc_graph *g = d->g;
+    const size_t n = g->n, RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32;
+    int rc = LDPC_OK;
+    for (int32_t c0 = 0, i = 0; c0 < B && rc == LDPC_OK; c0 += d->sub, i++) {
+        const int slot = i & 1;
+        const int32_t b = std::min(d->sub, B - c0);
+        cudaStream_t s = d->st[slot];
+        cudaError_t e = cudaMemcpyAsync(d->p[slot], p_host + (size_t)c0 * n, sizeof(double) * n * b,
+                                        cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) {
+            set_error("H2D priors: %s", cudaGetErrorString(e));
+            rc = LDPC_ECUDA;
+            break;
+        }
+        rc = ldpc_decode(g, d->p[slot], b, max_iterations, flags, d->est[slot], d->succ[slot], d->its[slot],
+                         syn_bits_host ? d->syn[slot] : nullptr, d->ws[slot], d->ws_bytes, s, nullptr);
+        if (rc) break;
+        e = cudaMemcpyAsync(est_bits_host + (size_t)c0 * RWn, d->est[slot], sizeof(uint32_t) * RWn * b,
+                            cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(success_host + c0, d->succ[slot], b, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(iters_host + c0, d->its[slot], sizeof(int32_t) * b, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && syn_bits_host)
+            e = cudaMemcpyAsync(syn_bits_host + (size_t)c0 * RWm, d->syn[slot], sizeof(uint32_t) * RWm * b,
+                                cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) {
+            set_error("D2H results: %s", cudaGetErrorString(e));
+            rc = LDPC_ECUDA;
+        }
+    }
+    for (int i = 0; i < 2; i++) {
+        cudaError_t e = cudaStreamSynchronize(d->st[i]);
+        if (e != cudaSuccess && rc == LDPC_OK) {
+            set_error("decode: %s", cudaGetErrorString(e));
+            rc = LDPC_ECUDA;
+        }
+    }
+    if (rc == LDPC_ECUDA) d->poisoned = true;  // mirrors engine.py:389-392: refuse further use
+    return rc;
+}
+
+extern "C" void ldpc_decoder_destroy(ldpc_decoder *d) { decoder_free(d); }

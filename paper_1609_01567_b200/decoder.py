@@ -1,0 +1,434 @@
+"""The decoder API of the reference, backed by the B200 kernels.
+
+Reference interface mirrored here (edgeldpc):
+  priors_awgn, initialize, MessageState, DecodeResult    serial.py:22-60
+  values_to_check / values_to_variable / estimate / syndrome  serial.py:63-147
+  decode_awgn                                            serial.py:150-178
+  ParallelDecoder(tables, group_size, n_threads).decode  engine.py:220-420
+  parallel_decode_awgn                                   engine.py:423-440
+
+Same names, argument meaning and errors (ValueError for sigma2 <= 0, length
+mismatches, negative max_iterations, group_size/n_threads < 1; RuntimeError
+after close).  Results are bit-identical to the reference on the same inputs.
+Added for throughput: ``ParallelDecoder.decode_batch`` (B frames per call,
+host buffers, pipelined copies) and ``decode_device`` (device tensors, for
+benchmarks and multi-GPU sharding).  ``group_size`` and ``n_threads`` are
+accepted for compatibility; the CUDA grid replaces the reference's pages and
+worker pool.
+
+Priors are computed on the host with the reference's own numpy expression
+(serial.py:49-50): numpy's exp is machine dependent in the last ulp, and bit
+parity requires the same priors, so they cross to the device as fp64.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .codes import ParityCheckMatrix
+from .tables import CodeTables
+
+DEFAULT_MAX_ITERATIONS = 50   # serial.py:19
+DEFAULT_GROUP_SIZE = 512      # engine.py:30
+
+
+@dataclass
+class MessageState:
+    """Priors p (per variable) and edge messages q, r (serial.py:22-28)."""
+
+    p: np.ndarray
+    q: np.ndarray
+    r: np.ndarray
+
+
+@dataclass
+class DecodeResult:
+    """serial.py:31-36."""
+
+    estimate: np.ndarray
+    success: bool
+    iterations_used: int
+    syndrome: np.ndarray
+
+
+def priors_awgn(y, sigma2: float) -> np.ndarray:
+    """P(bit = 1) for BPSK over AWGN, serial.py:39-50 (same numpy expression)."""
+    if sigma2 <= 0:
+        raise ValueError("sigma2 must be positive")
+    y = np.asarray(y, dtype=np.float64)
+    with np.errstate(over="ignore"):  # exp overflow saturates p to exactly 0.0
+        return 1.0 / (1.0 + np.exp(-2.0 * y / sigma2))
+
+
+_prior_pool = None
+
+
+def priors_awgn_batch(Y, sigma2, threads: int | None = None) -> np.ndarray:
+    """priors_awgn over a [B, n] batch, rows fanned out over host threads.
+
+    Element-wise identical to calling priors_awgn per frame (numpy's exp does
+    not depend on array position; tests/test_host.py pins this).  sigma2 may
+    be a scalar or a per-frame [B] array.
+    """
+    global _prior_pool
+    Y = np.ascontiguousarray(Y, dtype=np.float64)
+    if Y.ndim != 2:
+        raise ValueError("Y must be [B, n]")
+    s2 = np.broadcast_to(np.asarray(sigma2, dtype=np.float64), (Y.shape[0],))
+    if (s2 <= 0).any():
+        raise ValueError("sigma2 must be positive")
+    out = np.empty_like(Y)
+    nt = threads or min(32, os.cpu_count() or 1)
+    if nt <= 1 or Y.shape[0] == 1:
+        for b in range(Y.shape[0]):
+            out[b] = priors_awgn(Y[b], float(s2[b]))
+        return out
+    if _prior_pool is None:
+        _prior_pool = ThreadPoolExecutor(max_workers=nt)
+
+    def work(b):
+        with np.errstate(over="ignore"):
+            np.divide(1.0, 1.0 + np.exp(-2.0 * Y[b] / float(s2[b])), out=out[b])
+
+    list(_prior_pool.map(work, range(Y.shape[0])))
+    return out
+
+
+def initialize(y, sigma2: float, tables: CodeTables) -> MessageState:
+    """serial.py:53-60 (host): q copies each edge's prior, r starts at 1/2."""
+    p = priors_awgn(y, sigma2)
+    if len(p) != tables.n:
+        raise ValueError(f"expected {tables.n} observations, got {len(p)}")
+    return MessageState(p, p[tables.variable.v], np.full(tables.total_edges, 0.5))
+
+
+# ---- device plumbing ----------------------------------------------------------
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _workspace(graph, B: int):
+    torch = _torch()
+    nbytes = int(_native.lib().ldpc_workspace_bytes(graph.handle, int(B)))
+    return torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{graph.device}"), nbytes
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _tables_of(obj) -> CodeTables:
+    if isinstance(obj, CodeTables):
+        return obj
+    if isinstance(obj, ParityCheckMatrix):
+        cache = _H_TABLES.get(id(obj))
+        if cache is None or cache[0] is not obj:
+            cache = (obj, CodeTables.from_matrix(obj))
+            _H_TABLES[id(obj)] = cache
+        return cache[1]
+    raise TypeError("expected CodeTables or ParityCheckMatrix")
+
+
+_H_TABLES: dict = {}
+
+
+def _as_batch(a, width: int, what: str) -> tuple[np.ndarray, bool]:
+    a = np.asarray(a, dtype=np.float64)
+    single = a.ndim == 1
+    a2 = a.reshape(1, -1) if single else a
+    if a2.ndim != 2 or a2.shape[1] != width:
+        raise ValueError(f"expected {width} {what}, got {a.shape[-1] if a.ndim else 0}")
+    return np.ascontiguousarray(a2), single
+
+
+def _dev(a: np.ndarray, device: int):
+    return _torch().from_numpy(a).to(f"cuda:{device}")
+
+
+# ---- single phases (serial.py:63-147 signatures, any batch) -------------------
+
+def values_to_check(p, r, tables: CodeTables) -> np.ndarray:
+    """V-phase (serial.py:63-89) on the GPU; p [n] or [B,n], r [E] or [B,E] canonical order."""
+    T = _tables_of(tables)
+    P, single = _as_batch(p, T.n, "priors")
+    R, _ = _as_batch(r, T.total_edges, "messages")
+    if P.shape[0] != R.shape[0]:
+        raise ValueError("batch mismatch between p and r")
+    B = P.shape[0]
+    g = T.graph
+    torch = _torch()
+    ws, nb = _workspace(g, B)
+    dp, dr = _dev(P, g.device), _dev(R, g.device)
+    dq = torch.empty_like(dr)
+    _native.check(_native.lib().ldpc_phase_to_check(g.handle, _ptr(dp), _ptr(dr), _ptr(dq), B, _ptr(ws), nb,
+                                                    _native.current_stream_handle()), "values_to_check")
+    q = dq.cpu().numpy()
+    return q[0] if single else q
+
+
+def values_to_variable(q, tables: CodeTables) -> np.ndarray:
+    """C-phase (serial.py:92-112) on the GPU; q [E] or [B,E] canonical order."""
+    T = _tables_of(tables)
+    Q, single = _as_batch(q, T.total_edges, "messages")
+    B = Q.shape[0]
+    g = T.graph
+    torch = _torch()
+    ws, nb = _workspace(g, B)
+    dq = _dev(Q, g.device)
+    dr = torch.empty_like(dq)
+    _native.check(_native.lib().ldpc_phase_to_variable(g.handle, _ptr(dq), _ptr(dr), B, _ptr(ws), nb,
+                                                       _native.current_stream_handle()), "values_to_variable")
+    r = dr.cpu().numpy()
+    return r[0] if single else r
+
+
+def estimate(p, r, tables: CodeTables) -> np.ndarray:
+    """Hard decision (serial.py:115-133) on the GPU."""
+    T = _tables_of(tables)
+    P, single = _as_batch(p, T.n, "priors")
+    R, _ = _as_batch(r, T.total_edges, "messages")
+    B = P.shape[0]
+    g = T.graph
+    torch = _torch()
+    ws, nb = _workspace(g, B)
+    dp, dr = _dev(P, g.device), _dev(R, g.device)
+    dc = torch.empty((B, T.n), dtype=torch.uint8, device=dp.device)
+    _native.check(_native.lib().ldpc_phase_estimate(g.handle, _ptr(dp), _ptr(dr), _ptr(dc), B, _ptr(ws), nb,
+                                                    _native.current_stream_handle()), "estimate")
+    c = dc.cpu().numpy()
+    return c[0] if single else c
+
+
+def syndrome(c_hat, H) -> np.ndarray:
+    """z = H c_hat mod 2 (serial.py:136-147) on the GPU; H may be a ParityCheckMatrix or CodeTables."""
+    T = _tables_of(H)
+    c = np.asarray(c_hat)
+    single = c.ndim == 1
+    c2 = (c.reshape(1, -1) if single else c)
+    if c2.shape[-1] != T.n:
+        raise ValueError(f"estimate length {c2.shape[-1]} does not match n={T.n}")
+    c2 = np.ascontiguousarray(c2.astype(np.int64) & 1, dtype=np.uint8)
+    B = c2.shape[0]
+    g = T.graph
+    torch = _torch()
+    ws, nb = _workspace(g, B)
+    dc = _dev(c2, g.device)
+    dz = torch.empty((B, T.m), dtype=torch.uint8, device=dc.device)
+    _native.check(_native.lib().ldpc_phase_syndrome(g.handle, _ptr(dc), _ptr(dz), B, _ptr(ws), nb,
+                                                    _native.current_stream_handle()), "syndrome")
+    z = dz.cpu().numpy()
+    return z[0] if single else z
+
+
+# ---- batch results -------------------------------------------------------------
+
+def unpack_bits(words: np.ndarray, width: int) -> np.ndarray:
+    """[B, ceil(width/32)] uint32 little-bit-order rows -> [B, width] uint8."""
+    w = np.ascontiguousarray(words, dtype=np.uint32)
+    return np.unpackbits(w.view(np.uint8), axis=-1, bitorder="little")[..., :width]
+
+
+class BatchResult:
+    """Results of B frames: packed estimate/syndrome bits, flags and counts."""
+
+    def __init__(self, est_bits, success, iterations, syn_bits, n: int, m: int):
+        self.est_bits = est_bits
+        self.success = success
+        self.iterations = iterations
+        self.syn_bits = syn_bits
+        self.n, self.m = n, m
+
+    def __len__(self) -> int:
+        return len(self.success)
+
+    def estimates(self) -> np.ndarray:
+        return unpack_bits(self.est_bits, self.n)
+
+    def syndromes(self) -> np.ndarray:
+        return unpack_bits(self.syn_bits, self.m)
+
+    def __getitem__(self, i: int) -> DecodeResult:
+        return DecodeResult(unpack_bits(self.est_bits[i:i + 1], self.n)[0], bool(self.success[i]),
+                            int(self.iterations[i]), unpack_bits(self.syn_bits[i:i + 1], self.m)[0])
+
+
+# ---- the decoder ----------------------------------------------------------------
+
+class ParallelDecoder:
+    """GPU drop-in for edgeldpc.engine.ParallelDecoder (engine.py:220-420).
+
+    One instance owns a device decode context for up to ``max_batch`` frames
+    (pipelined host<->device copies over two streams).  Reentrant use from
+    several threads is serialised by the native context (engine.py:223-226
+    allows concurrent decode calls on one n_threads == 1 instance).
+    """
+
+    def __init__(self, tables, group_size: int = DEFAULT_GROUP_SIZE, n_threads: int = 1, *,
+                 max_batch: int = 1024, sub_batch: int = 0):
+        if group_size < 1:
+            raise ValueError("group_size must be at least 1")      # engine.py:51-52
+        if n_threads < 1:
+            raise ValueError("n_threads must be at least 1")       # engine.py:234-235
+        if max_batch < 1:
+            raise ValueError("max_batch must be at least 1")
+        self.tables = _tables_of(tables)
+        self.group_size = group_size
+        self.n_threads = n_threads
+        self.max_batch = int(max_batch)
+        L = _native.lib()
+        h = ctypes.c_void_p()
+        _native.check(L.ldpc_decoder_create(self.tables.graph.handle, self.max_batch, int(sub_batch),
+                                            ctypes.byref(h)), "ldpc_decoder_create")
+        self._h = h
+        self._closed = False
+        self._lock = threading.Lock()
+
+    # engine.py:363-398
+    def decode(self, y, sigma2: float, max_iterations: int = DEFAULT_MAX_ITERATIONS) -> DecodeResult:
+        if self._closed:
+            raise RuntimeError("decoder is closed")
+        if max_iterations < 0:
+            raise ValueError("max_iterations must be non-negative")
+        p = priors_awgn(y, sigma2)
+        if p.ndim != 1 or len(p) != self.tables.n:
+            raise ValueError(f"expected {self.tables.n} observations, got {len(p)}")
+        return self.decode_priors(p.reshape(1, -1), max_iterations)[0]
+
+    def decode_batch(self, Y, sigma2, max_iterations: int = DEFAULT_MAX_ITERATIONS,
+                     early_stop: bool = True) -> BatchResult:
+        """B received frames [B, n] (sigma2 scalar or [B]) -> BatchResult."""
+        if self._closed:
+            raise RuntimeError("decoder is closed")
+        Y = np.asarray(Y, dtype=np.float64)
+        if Y.ndim != 2 or Y.shape[1] != self.tables.n:
+            raise ValueError(f"expected frames of {self.tables.n} observations")
+        return self.decode_priors(priors_awgn_batch(Y, sigma2), max_iterations, early_stop)
+
+    def decode_priors(self, P, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
+                      out: BatchResult | None = None) -> BatchResult:
+        """Host priors [B, n] (pinned memory recommended) -> host BatchResult."""
+        if self._closed:
+            raise RuntimeError("decoder is closed")
+        if max_iterations < 0:
+            raise ValueError("max_iterations must be non-negative")
+        P = np.ascontiguousarray(P, dtype=np.float64)
+        if P.ndim != 2 or P.shape[1] != self.tables.n:
+            raise ValueError(f"expected priors of shape [B, {self.tables.n}]")
+        B = P.shape[0]
+        n, m = self.tables.n, self.tables.m
+        res = out if out is not None else BatchResult(np.empty((B, (n + 31) // 32), np.uint32),
+                                                      np.empty(B, np.uint8), np.empty(B, np.int32),
+                                                      np.empty((B, (m + 31) // 32), np.uint32), n, m)
+        L = _native.lib()
+        flags = _native.FLAG_EARLY_STOP if early_stop else _native.FLAG_FIXED_ITERS
+        with self._lock:
+            for c0 in range(0, B, self.max_batch):
+                c1 = min(B, c0 + self.max_batch)
+                rc = L.ldpc_decoder_decode_host(
+                    self._h, P[c0:c1].ctypes.data, c1 - c0, int(max_iterations), flags,
+                    res.est_bits[c0:c1].ctypes.data, res.success[c0:c1].ctypes.data,
+                    res.iterations[c0:c1].ctypes.data, res.syn_bits[c0:c1].ctypes.data)
+                if rc == _native.LDPC_ECUDA or rc == _native.LDPC_ECLOSED:
+                    self._closed = True   # engine.py:389-392: poisoned after a device fault
+                _native.check(rc, "decode")
+        return res
+
+    def decode_device(self, P_dev, max_iterations: int, early_stop: bool = True, workspace=None,
+                      outputs=None, profile: "_native.Profile | None" = None, syndrome_out: bool = True):
+        """Device priors tensor [B, n] fp64 -> device tensors (est_bits, success, iters, syn_bits).
+
+        Stream-ordered on torch's current stream; no host synchronisation
+        unless ``profile`` is given (event timings are resolved at the end).
+        """
+        if self._closed:
+            raise RuntimeError("decoder is closed")
+        torch = _torch()
+        g = self.tables.graph
+        B = int(P_dev.shape[0])
+        if P_dev.dtype != torch.float64 or P_dev.dim() != 2 or P_dev.shape[1] != g.n or not P_dev.is_contiguous():
+            raise ValueError("P_dev must be a contiguous float64 [B, n] CUDA tensor")
+        if workspace is None:
+            workspace, nb = _workspace(g, B)
+        else:
+            nb = workspace.numel()
+        if outputs is None:
+            outputs = self.alloc_outputs(B, P_dev.device)
+        est, ok, its, syn = outputs
+        flags = _native.FLAG_EARLY_STOP if early_stop else _native.FLAG_FIXED_ITERS
+        rc = _native.lib().ldpc_decode(g.handle, _ptr(P_dev), B, int(max_iterations), flags, _ptr(est), _ptr(ok),
+                                       _ptr(its), _ptr(syn) if syndrome_out else None, _ptr(workspace), nb,
+                                       _native.current_stream_handle(),
+                                       ctypes.byref(profile) if profile is not None else None)
+        _native.check(rc, "ldpc_decode")
+        return outputs
+
+    def alloc_outputs(self, B: int, device):
+        torch = _torch()
+        n, m = self.tables.n, self.tables.m
+        return (torch.empty((B, (n + 31) // 32), dtype=torch.int32, device=device),
+                torch.empty(B, dtype=torch.uint8, device=device),
+                torch.empty(B, dtype=torch.int32, device=device),
+                torch.empty((B, (m + 31) // 32), dtype=torch.int32, device=device))
+
+    def workspace(self, B: int):
+        return _workspace(self.tables.graph, B)[0]
+
+    def count_errors(self, outputs, counts_dev):
+        """Accumulate [bit errors, failures, iterations, frames] (all-zero codeword) into int64[4]."""
+        est, ok, its, _ = outputs
+        rc = _native.lib().ldpc_count_errors(self.tables.graph.handle, _ptr(est), _ptr(ok), _ptr(its),
+                                             int(ok.shape[0]), _ptr(counts_dev), _native.current_stream_handle())
+        _native.check(rc, "ldpc_count_errors")
+
+    # engine.py:400-420
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _native.load_library().ldpc_decoder_destroy(self._h)
+            self._h = None
+        self._closed = True
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+GpuDecoder = ParallelDecoder
+
+
+def decode_awgn(y, sigma2: float, max_iterations: int, tables, H: ParityCheckMatrix | None = None) -> DecodeResult:
+    """serial.py:150-178 signature, decoded on the GPU."""
+    if max_iterations < 0:
+        raise ValueError("max_iterations must be non-negative")
+    T = _tables_of(tables)
+    if H is not None and (H.n != T.n or H.m != T.m):
+        raise ValueError("H does not match the tables")
+    with ParallelDecoder(T, max_batch=1) as dec:
+        return dec.decode(y, sigma2, max_iterations)
+
+
+def parallel_decode_awgn(y, sigma2: float, max_iterations: int, tables, H: ParityCheckMatrix | None = None,
+                         group_size: int = DEFAULT_GROUP_SIZE, n_threads: int = 1) -> DecodeResult:
+    """engine.py:423-440: one-shot decode through a throwaway decoder."""
+    T = _tables_of(tables)
+    if H is not None and (H.n != T.n or H.m != T.m):
+        raise ValueError("H does not match the tables")
+    with ParallelDecoder(T, group_size=group_size, n_threads=n_threads, max_batch=1) as dec:
+        return dec.decode(y, sigma2, max_iterations)

@@ -1,0 +1,196 @@
+"""End-to-end decode parity (serial.py:150-178, engine.py:363-440), bit-exact.
+
+Estimates, success flags, iteration counts and syndromes must equal the
+reference's on the same priors: golden fixtures from running the reference,
+the CPU oracle on batches of every BASELINE config, and size-independent
+properties at full size."""
+
+import numpy as np
+import pytest
+
+from conftest import PAIRS_14_7, golden_code
+from paper_1609_01567_b200 import (
+    CodeTables,
+    ParallelDecoder,
+    ParityCheckMatrix,
+    decode_awgn,
+    parallel_decode_awgn,
+    priors_awgn_batch,
+    syndrome,
+)
+from paper_1609_01567_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(code, B, ebno_db, seed):
+    H = configs.code(code)
+    s2 = configs.ebno_to_sigma2(ebno_db, configs.rate(H))
+    rng = np.random.default_rng(seed)
+    return H, priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((B, H.n)), s2)
+
+
+def test_golden_decode(cuda, golden_tables, golden_decode):
+    for key in golden_decode["cases"]:
+        code = str(golden_decode[f"{key}/code"])
+        T = CodeTables.from_matrix(golden_code(golden_tables, code))
+        it = int(golden_decode[f"{key}/max_iterations"])
+        P = golden_decode[f"{key}/p"]
+        with ParallelDecoder(T, max_batch=len(P)) as dec:
+            res = dec.decode_priors(P, it)
+        assert np.array_equal(res.estimates(), golden_decode[f"{key}/estimate"]), key
+        assert np.array_equal(res.success.astype(bool), golden_decode[f"{key}/success"]), key
+        assert np.array_equal(res.iterations, golden_decode[f"{key}/iterations"]), key
+        assert np.array_equal(res.syndromes(), golden_decode[f"{key}/syndrome"]), key
+
+
+def test_golden_fixed_iterations(cuda, golden_tables, golden_decode):
+    T = CodeTables.from_matrix(golden_code(golden_tables, "c1"))
+    P = golden_decode["fixed/p"]
+    with ParallelDecoder(T, max_batch=len(P)) as dec:
+        res = dec.decode_priors(P, int(golden_decode["fixed/max_iterations"]), early_stop=False)
+    assert np.array_equal(res.estimates(), golden_decode["fixed/estimate"])
+    assert np.array_equal(res.success.astype(bool), golden_decode["fixed/success"])
+    assert np.array_equal(res.syndromes(), golden_decode["fixed/syndrome"])
+    assert (res.iterations == 10).all()
+
+
+def test_single_frame_api_matches_golden(cuda, golden_tables, golden_decode):
+    # the reference's call shapes: decode_awgn / parallel_decode_awgn / ParallelDecoder.decode from y
+    H = golden_code(golden_tables, "h14")
+    T = CodeTables.from_matrix(H)
+    for key in ("h14_s05", "h14_s10"):
+        Y = golden_decode[f"{key}/y"]
+        s2 = float(golden_decode[f"{key}/sigma2"])
+        it = int(golden_decode[f"{key}/max_iterations"])
+        with ParallelDecoder(T) as dec:
+            for i, y in enumerate(Y):
+                for res in (decode_awgn(y, s2, it, T, H), parallel_decode_awgn(y, s2, it, T, H),
+                            dec.decode(y, s2, it)):
+                    assert np.array_equal(res.estimate, golden_decode[f"{key}/estimate"][i])
+                    assert res.success == bool(golden_decode[f"{key}/success"][i])
+                    assert res.iterations_used == int(golden_decode[f"{key}/iterations"][i])
+                    assert np.array_equal(res.syndrome, golden_decode[f"{key}/syndrome"][i])
+
+
+@pytest.mark.parametrize("code,B,ebno,iters,early", [
+    ("C1", 70, 2.0, 50, True),
+    ("C1", 33, 1.0, 50, True),
+    ("C2", 64, 2.0, 20, True),
+    ("C2", 40, 1.5, 20, False),
+    ("C4", 24, 2.0, 20, True),
+    ("C4", 20, 1.0, 8, False),
+])
+def test_batches_vs_oracle(cuda, code, B, ebno, iters, early):
+    from oracle import OracleTables
+
+    H, P = _frames(code, B, ebno, seed=B * 7 + iters)
+    T = CodeTables.from_matrix(H)
+    with ParallelDecoder(T, max_batch=B, sub_batch=32) as dec:
+        res = dec.decode_priors(P, iters, early_stop=early)
+    est, ok, its, z = OracleTables.from_matrix(H).decode_batch(P, iters, fixed_iterations=not early)
+    assert np.array_equal(res.estimates(), est)
+    assert np.array_equal(res.success.astype(bool), ok)
+    assert np.array_equal(res.iterations, its)
+    assert np.array_equal(res.syndromes(), z)
+
+
+def test_device_path_equals_host_path(cuda):
+    import torch
+
+    H, P = _frames("C2", 96, 1.8, seed=3)
+    T = CodeTables.from_matrix(H)
+    with ParallelDecoder(T, max_batch=96) as dec:
+        host = dec.decode_priors(P, 20)
+        est, ok, its, syn = dec.decode_device(torch.from_numpy(P).cuda(), 20)
+        torch.cuda.synchronize()
+    assert np.array_equal(est.cpu().numpy().view(np.uint32), host.est_bits)
+    assert np.array_equal(ok.cpu().numpy(), host.success)
+    assert np.array_equal(its.cpu().numpy(), host.iterations)
+    assert np.array_equal(syn.cpu().numpy().view(np.uint32), host.syn_bits)
+
+
+def test_edge_cases(cuda):
+    from oracle import OracleTables
+
+    H = ParityCheckMatrix(14, 7, PAIRS_14_7)
+    T = CodeTables.from_matrix(H)
+    O = OracleTables.from_matrix(H)
+    rng = np.random.default_rng(5)
+    with ParallelDecoder(T, max_batch=130, sub_batch=64) as dec:
+        for B in (1, 31, 32, 33, 64, 65, 130):
+            P = priors_awgn_batch(-1.0 + 1.2 * rng.standard_normal((B, 14)), 0.9)
+            for it in (0, 1, 7):
+                for early in (True, False):
+                    res = dec.decode_priors(P, it, early_stop=early)
+                    est, ok, its, z = O.decode_batch(P, it, fixed_iterations=not early)
+                    assert np.array_equal(res.estimates(), est), (B, it, early)
+                    assert np.array_equal(res.success.astype(bool), ok), (B, it, early)
+                    assert np.array_equal(res.iterations, its), (B, it, early)
+                    assert np.array_equal(res.syndromes(), z), (B, it, early)
+        # saturated priors (p = 0 / 1 / 0.5) survive the kernels exactly like the reference
+        P = np.array([[0.0, 1.0, 0.5] * 4 + [0.0, 1.0]] * 3)
+        res = dec.decode_priors(P, 5)
+        est, ok, its, z = O.decode_batch(P, 5)
+        assert np.array_equal(res.estimates(), est) and np.array_equal(res.iterations, its)
+
+
+def test_errors_mirror_reference(cuda):
+    H = ParityCheckMatrix(14, 7, PAIRS_14_7)
+    T = CodeTables.from_matrix(H)
+    with pytest.raises(ValueError):
+        ParallelDecoder(T, group_size=0)
+    with pytest.raises(ValueError):
+        ParallelDecoder(T, n_threads=0)
+    dec = ParallelDecoder(T)
+    with pytest.raises(ValueError):
+        dec.decode(np.zeros(14), 0.0, 5)
+    with pytest.raises(ValueError):
+        dec.decode(np.zeros(13), 1.0, 5)
+    with pytest.raises(ValueError):
+        dec.decode(np.zeros(14), 1.0, -1)
+    dec.close()
+    with pytest.raises(RuntimeError):
+        dec.decode(np.zeros(14), 1.0, 5)
+    with pytest.raises(ValueError):
+        parallel_decode_awgn(np.zeros(14), 1.0, 5, T, ParityCheckMatrix(3, 2, ((0, 0), (0, 1), (1, 1), (1, 2))))
+
+
+def test_clean_codeword_zero_iterations(cuda):
+    H = ParityCheckMatrix(14, 7, PAIRS_14_7)
+    T = CodeTables.from_matrix(H)
+    for gain in (1.0, 0.25, 3.7):
+        res = decode_awgn(np.full(14, -gain), 0.4, 50, T, H)
+        assert res.success and res.iterations_used == 0 and not res.estimate.any() and not res.syndrome.any()
+
+
+@pytest.mark.slow
+def test_dvbs2_full_batch(cuda):
+    """BASELINE config C3 at full size: 1024 codewords, fixed 10 iterations.
+
+    Sampled codewords are compared bit-exactly with the oracle; every codeword
+    is checked against size-independent properties (syndrome == H * estimate,
+    success <=> zero syndrome, iteration count)."""
+    from oracle import OracleTables
+
+    H, P = _frames("C3", 1024, 2.0, seed=64800)
+    T = CodeTables.from_matrix(H)
+    with ParallelDecoder(T, max_batch=1024) as dec:
+        res = dec.decode_priors(P, 10, early_stop=False)
+    est = res.estimates()
+    z = res.syndromes()
+    assert np.array_equal(syndrome(est[:64], T), z[:64])
+    assert np.array_equal(res.success.astype(bool), ~z.any(axis=1))
+    assert (res.iterations == 10).all()
+    sample = np.arange(0, 1024, 37)
+    e_o, ok_o, it_o, z_o = OracleTables.from_matrix(H).decode_batch(P[sample], 10, fixed_iterations=True)
+    assert np.array_equal(est[sample], e_o)
+    assert np.array_equal(z[sample], z_o)
+    assert np.array_equal(res.success[sample].astype(bool), ok_o)
+    # early-stop mode on the same frames: the reference's semantics
+    with ParallelDecoder(T, max_batch=1024) as dec:
+        res2 = dec.decode_priors(P, 10, early_stop=True)
+    e2, ok2, it2, z2 = OracleTables.from_matrix(H).decode_batch(P[sample], 10)
+    assert np.array_equal(res2.estimates()[sample], e2)
+    assert np.array_equal(res2.iterations[sample], it2)
+    assert np.array_equal(res2.success[sample].astype(bool), ok2)

@@ -1,0 +1,165 @@
+"""Per-phase parity of the CUDA kernels (serial.py:63-147), bit-exact.
+
+Against (a) the reference's outputs (golden fixtures), (b) the CPU oracle on
+random batched states of the full-size configs, and (c) the reference's own
+phase KATs (test_serial.py:66-181)."""
+
+import numpy as np
+import pytest
+
+from conftest import PAIRS_14_7, dense_syndrome, golden_code, random_parity_matrix
+from paper_1609_01567_b200 import (
+    CodeTables,
+    ParityCheckMatrix,
+    estimate,
+    syndrome,
+    values_to_check,
+    values_to_variable,
+)
+from paper_1609_01567_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def tables14(cuda):
+    return CodeTables.from_matrix(ParityCheckMatrix(14, 7, PAIRS_14_7))
+
+
+@pytest.fixture(scope="module")
+def chain3(cuda):
+    H = ParityCheckMatrix(3, 2, ((0, 0), (0, 1), (1, 1), (1, 2)))
+    return H, CodeTables.from_matrix(H)
+
+
+def test_golden_phases(cuda, golden_tables, golden_phases):
+    for name in golden_phases["names"]:
+        H = golden_code(golden_tables, name)
+        T = CodeTables.from_matrix(H)
+        g = lambda k: golden_phases[f"{name}/{k}"]  # noqa: E731
+        # batched over the S states at once, and one state at a time
+        assert np.array_equal(bits(values_to_check(g("p"), g("r"), T)), bits(g("to_check"))), name
+        assert np.array_equal(bits(values_to_variable(g("q"), T)), bits(g("to_variable"))), name
+        assert np.array_equal(estimate(g("p"), g("r"), T), g("estimate")), name
+        assert np.array_equal(syndrome(g("chat_in"), T), g("syndrome")), name
+        assert np.array_equal(bits(values_to_variable(g("q")[1], T)), bits(g("to_variable")[1])), name
+
+
+@pytest.mark.parametrize("code,B", [("C1", 5), ("C2", 3), ("C3", 2), ("C4", 3)])
+def test_random_states_vs_oracle(cuda, code, B):
+    from oracle import OracleTables
+
+    H = configs.code(code)
+    T = CodeTables.from_matrix(H)
+    O = OracleTables.from_matrix(H)
+    rng = np.random.default_rng(sum(map(ord, code)))
+    P = rng.uniform(size=(B, H.n))
+    R = rng.uniform(size=(B, H.total_edges))
+    Q = rng.uniform(size=(B, H.total_edges))
+    C = rng.integers(0, 2, size=(B, H.n)).astype(np.uint8)
+    q = values_to_check(P, R, T)
+    r = values_to_variable(Q, T)
+    c = estimate(P, R, T)
+    z = syndrome(C, T)
+    for b in range(B):
+        assert np.array_equal(bits(q[b]), bits(O.values_to_check(P[b], R[b]))), (code, b)
+        assert np.array_equal(bits(r[b]), bits(O.values_to_variable(Q[b]))), (code, b)
+        assert np.array_equal(c[b], O.estimate(P[b], R[b])), (code, b)
+        assert np.array_equal(z[b], O.syndrome(C[b])), (code, b)
+
+
+# ---- test_serial.py KATs, run on the GPU kernels ----------------------------
+
+class TestValuesToCheck:
+    def test_degree_one_variable_passes_prior(self, chain3):
+        _, T = chain3
+        q = values_to_check(np.array([0.3, 0.6, 0.9]), np.array([0.1, 0.2, 0.3, 0.4]), T)
+        assert q[int(np.flatnonzero(T.variable.v == 0)[0])] == 0.3
+        assert q[int(np.flatnonzero(T.variable.v == 2)[0])] == 0.9
+
+    def test_uniform_messages_return_prior(self, tables14):
+        p = np.linspace(0.05, 0.95, 14)
+        q = values_to_check(p, np.full(31, 0.5), tables14)
+        assert q == pytest.approx(p[tables14.variable.v], abs=1e-15)
+
+    def test_two_term_product(self, chain3):
+        _, T = chain3
+        q = values_to_check(np.full(3, 0.5), np.full(4, 0.8), T)
+        for k in np.flatnonzero(T.variable.v == 1):
+            assert q[k] == pytest.approx(0.8, abs=1e-15)
+
+    def test_double_underflow_saturates(self, chain3):
+        _, T = chain3
+        q = values_to_check(np.array([0.5, 1.0, 0.5]), np.zeros(4), T)
+        assert q[int(np.flatnonzero(T.variable.v == 1)[0])] == 0.5
+
+    def test_messages_stay_in_unit_interval(self, tables14):
+        rng = np.random.default_rng(3)
+        q = values_to_check(rng.uniform(size=(50, 14)), rng.uniform(size=(50, 31)), tables14)
+        assert ((0.0 <= q) & (q <= 1.0)).all()
+
+
+class TestValuesToVariable:
+    def test_degree_two_check_reproduces_reference_rounding(self, chain3):
+        # serial.py:111 evaluates 1-(0.5+0.5*(1-2q)); for q=0.2 that is 0.19999999999999996,
+        # not 0.2 (the reference's own test_serial.py:113-123 expects 0.2 and fails on the
+        # reference): the kernel must reproduce the reference arithmetic, not "fix" it.
+        _, T = chain3
+        q = np.array([0.2, 0.7, 0.6, 0.9])
+        r = values_to_variable(q, T)
+        chk = T.check
+        for pos in range(4):
+            target = int(chk.e[pos])
+            group = [int(chk.e[i]) for i in range(int(chk.s[pos]), int(chk.s[pos]) + 2)]
+            other = next(g for g in group if g != target)
+            assert r[target] == 1.0 - (0.5 + 0.5 * (1.0 - 2.0 * q[other]))
+
+    def test_erasure_annihilates(self, tables14):
+        assert (values_to_variable(np.full(31, 0.5), tables14) == 0.5).all()
+
+    def test_certain_zero_neighbors(self, tables14):
+        assert (values_to_variable(np.zeros(31), tables14) == 0.0).all()
+
+    def test_range_property(self, tables14):
+        rng = np.random.default_rng(4)
+        r = values_to_variable(rng.uniform(size=(50, 31)), tables14)
+        assert ((0.0 <= r) & (r <= 1.0)).all()
+
+
+class TestEstimate:
+    def test_single_edge_decision(self, chain3):
+        _, T = chain3
+        r = np.full(4, 0.5)
+        r[int(np.flatnonzero(T.variable.v == 0)[0])] = 0.8
+        assert estimate(np.full(3, 0.5), r, T)[0] == 1
+
+    def test_uniform_messages_decide_by_prior(self, tables14):
+        assert (estimate(np.full(14, 0.3), np.full(31, 0.5), tables14) == 0).all()
+
+    def test_exact_tie_decides_one(self, tables14):
+        assert (estimate(np.full(14, 0.5), np.full(31, 0.5), tables14) == 1).all()
+
+
+class TestSyndrome:
+    def test_all_zero(self, tables14):
+        assert not syndrome(np.zeros(14, dtype=np.uint8), tables14).any()
+
+    def test_unit_vector_lights_adjacent_checks(self, tables14):
+        c = np.zeros(14, dtype=np.uint8)
+        c[0] = 1
+        assert sorted(np.flatnonzero(syndrome(c, tables14)).tolist()) == [0, 2, 3, 5]
+
+    def test_against_dense_oracle(self, cuda):
+        rng = np.random.default_rng(12)
+        for _ in range(50):
+            H = random_parity_matrix(rng)
+            c = rng.integers(0, 2, size=(3, H.n)).astype(np.uint8)
+            assert np.array_equal(syndrome(c, H), dense_syndrome(H, c))
+
+    def test_length_mismatch(self, tables14):
+        with pytest.raises(ValueError):
+            syndrome(np.zeros(13, dtype=np.uint8), tables14)
