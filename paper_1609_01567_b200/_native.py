@@ -73,6 +73,8 @@ def _declare(L):
     L.ldpc_decoder_decode_host.argtypes = [vp, vp, i32, i32, u32, vp, vp, vp, vp]
     L.ldpc_decoder_destroy.argtypes = [vp]
     L.ldpc_decoder_destroy.restype = None
+    L.ldpc_selftest_division.argtypes = [ctypes.c_uint64, i64, P_i64]
+    L.ldpc_selftest_division.restype = ctypes.c_int
     for name in ("ldpc_graph_create", "ldpc_graph_info", "ldpc_graph_get_tables", "ldpc_graph_get_var_groups",
                  "ldpc_graph_get_buckets", "ldpc_decode", "ldpc_count_errors", "ldpc_phase_to_check",
                  "ldpc_phase_to_variable", "ldpc_phase_estimate", "ldpc_phase_syndrome", "ldpc_decoder_create",

@@ -25,6 +25,15 @@ namespace {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 }  // namespace
 
+// LDPC_KERNEL=pipe selects the bulk-copy ring kernels (A/B comparisons); default: register loads
+bool use_pipe_kernels() {
+    static const bool pipe = [] {
+        const char *e = getenv("LDPC_KERNEL");
+        return e && std::string(e) == "pipe";
+    }();
+    return pipe;
+}
+
 size_t workspace_bytes(const ldpc_graph *g, int32_t B) {
     const size_t Bp = (size_t)padded_batch(B), NW = Bp / 32;
     size_t b = 0;
@@ -123,11 +132,13 @@ struct Prof {
     } while (0)
 
 NodeLaunch check_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
-    return NodeLaunch{g->chk_off, g->chk_var, g->chk_order, 0, 0, w.msg, w.P, nullptr, done, w.Bp, w.NW};
+    return NodeLaunch{g->chk_off, g->chk_var, g->chk_order, 0, 0, w.msg, w.P, nullptr, done, w.Bp, w.NW,
+                      (int32_t)g->E, g->n, g->chk_slot, g->chk_slot_ord, g->chk_var_ord, 0};
 }
 
 NodeLaunch var_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
-    return NodeLaunch{g->var_off, g->var_pos, g->var_order, 0, 0, w.msg, w.P, w.chat, done, w.Bp, w.NW};
+    return NodeLaunch{g->var_off, nullptr, g->var_order, 0, 0, w.msg, w.P, w.chat, done, w.Bp, w.NW,
+                      (int32_t)g->E, g->n, g->var_slot, g->var_slot_ord, nullptr, 0};
 }
 
 int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const uint32_t *done, cudaStream_t s) {
@@ -137,7 +148,9 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
         if (b.deg <= kMaxRegDegree) {
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
-            int rc = launch_check_bucket(a, b.deg, from_prior, s);
+            a.edge_begin = b.edge_begin;
+            int rc = use_pipe_kernels() ? launch_check_pipe(a, b.deg, from_prior, s)
+                                        : launch_check_bucket(a, b.deg, from_prior, s);
             if (rc) return rc;
         } else {
             if (wide_begin < 0) wide_begin = b.node_begin;
@@ -160,7 +173,9 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
         if (b.deg <= kMaxRegDegree) {
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
-            int rc = launch_var_bucket(a, b.deg, write_q, s);
+            a.edge_begin = b.edge_begin;
+            int rc = use_pipe_kernels() ? launch_var_pipe(a, b.deg, write_q, s)
+                                        : launch_var_bucket(a, b.deg, write_q, s);
             if (rc) return rc;
         } else {
             if (wide_begin < 0) wide_begin = b.node_begin;

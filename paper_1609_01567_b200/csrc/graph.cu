@@ -308,14 +308,62 @@ int build_buckets(const int32_t *deg_dev, int32_t count, int32_t *order_dev, std
         int32_t d = (int32_t)(host[i] >> 32);
         int32_t j = i;
         while (j < count && (int32_t)(host[j] >> 32) == d) j++;
-        buckets->push_back(Bucket{d, i, j - i});
+        const int32_t eb = buckets->empty() ? 0 : buckets->back().edge_begin + buckets->back().deg * buckets->back().node_count;
+        buckets->push_back(Bucket{d, i, j - i, eb});
         i = j;
     }
     return LDPC_OK;
 }
 
+__global__ void k_deg_by_order(const int32_t *order, const int32_t *off, int32_t count, int32_t *deg_ord) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t node = order[k];
+        deg_ord[k] = off[node + 1] - off[node];
+    }
+}
+
+__global__ void k_fill_ord(const int32_t *order, const int32_t *off, int32_t count, const int32_t *ord_off,
+                           const int32_t *slot, const int32_t *aux, int32_t *slot_ord, int32_t *aux_ord) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t node = order[k];
+        const int32_t a = off[node], d = off[node + 1] - a, o = ord_off[k];
+        for (int32_t i = 0; i < d; i++) {
+            slot_ord[o + i] = slot ? slot[a + i] : a + i;
+            if (aux_ord) aux_ord[o + i] = aux[a + i];
+        }
+    }
+}
+
+// Flat bucket-ordered edge tables of one side (see ldpc_graph::*_ord).
+int build_ord(const int32_t *order, int32_t count, const int32_t *off, const int32_t *slot, const int32_t *aux,
+              int64_t E, int32_t *tmp, int32_t **slot_ord, int32_t **aux_ord, cudaStream_t s) {
+    int32_t *deg_ord = nullptr, *ord_off = nullptr;
+    int rc = dalloc(&deg_ord, count);
+    if (!rc) rc = dalloc(&ord_off, (size_t)count + 1);
+    if (!rc) rc = dalloc(slot_ord, E);
+    if (!rc && aux_ord) rc = dalloc(aux_ord, E);
+    if (!rc) {
+        k_deg_by_order<<<grid_for(count), 256, 0, s>>>(order, off, count, deg_ord);
+        rc = cudaGetLastError() == cudaSuccess ? LDPC_OK : LDPC_ECUDA;
+    }
+    if (!rc) rc = exclusive_scan(deg_ord, ord_off, count, tmp, s);
+    if (!rc) {
+        k_fill_ord<<<grid_for(count), 256, 0, s>>>(order, off, count, ord_off, slot, aux, *slot_ord,
+                                                   aux_ord ? *aux_ord : nullptr);
+        rc = cudaGetLastError() == cudaSuccess ? LDPC_OK : LDPC_ECUDA;
+    }
+    if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = LDPC_ECUDA;
+    if (rc == LDPC_ECUDA) set_error("flat edge tables: %s", cudaGetErrorString(cudaGetLastError()));
+    cudaFree(deg_ord);
+    cudaFree(ord_off);
+    return rc;
+}
+
 void free_graph(ldpc_graph *g) {
     if (!g) return;
+    cudaFree(g->var_slot_ord);
+    cudaFree(g->chk_slot_ord);
+    cudaFree(g->chk_var_ord);
     cudaFree(g->var_off);
     cudaFree(g->var_pos);
     cudaFree(g->var_chk);
@@ -441,6 +489,16 @@ extern "C" int ldpc_graph_create(int32_t n, int32_t m, int64_t nnz, const int32_
     G1_TRY(build_buckets(var_deg, n, g->var_order, &g->var_buckets, s));
     G1_TRY(build_buckets(chk_deg, m, g->chk_order, &g->chk_buckets, s));
     G1_CUDA(cudaStreamSynchronize(s));
+    {
+        // LDPC_SLOTS=var: variable-major message slots (A/B layout experiments); default check-major
+        const char *lay = getenv("LDPC_SLOTS");
+        g->var_major = lay && std::string(lay) == "var";
+        g->chk_slot = g->var_major ? g->chk_edge : nullptr;
+        g->var_slot = g->var_major ? nullptr : g->var_pos;
+    }
+    G1_TRY(build_ord(g->var_order, n, g->var_off, g->var_slot, nullptr, nnz, tmp, &g->var_slot_ord, nullptr, s));
+    G1_TRY(build_ord(g->chk_order, m, g->chk_off, g->chk_slot, g->chk_var, nnz, tmp, &g->chk_slot_ord,
+                     &g->chk_var_ord, s));
 #undef G1_TRY
 #undef G1_CUDA
     fail(LDPC_OK);  // frees the temporaries only

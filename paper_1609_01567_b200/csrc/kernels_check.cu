@@ -12,11 +12,12 @@
 // to the CPython reference.
 //
 // Work mapping: one warp = one check node x 32*V codewords (lane = V adjacent
-// codewords, V = 2 -> 16-byte loads).  The q/r message of slot pos for
-// codeword c lives at msg[pos * Bp + c]: a warp's access per edge is one
-// contiguous 256*V-byte run, and the eight warps of a block take consecutive
-// codeword chunks of the same node.  The update is in place (q read, r
-// written to the same slots): each slot belongs to exactly one check.
+// codewords, V = 2 -> 16-byte loads).  Messages are chunk-major
+// (msg[c/64][slot][c%64], common.cuh): a warp's access per edge is one
+// contiguous 256*V-byte run, a check's d slots are adjacent, and the grid
+// sweeps all nodes of one codeword chunk before the next so the concurrently
+// touched window stays small.  The update is in place (q read, r written to
+// the same slots): each slot belongs to exactly one check.
 #include "common.cuh"
 
 namespace ldpc {
@@ -70,13 +71,17 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
     const int lane = threadIdx.x & 31;
     const int chunks = a.Bp / (32 * V);
     const int64_t task = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    const int ni = (int)(task / chunks);
-    const int ch = (int)(task - (int64_t)ni * chunks);
-    if (ni >= a.node_count) return;
+    // chunk-major sweep: all nodes of codeword chunk 0, then chunk 1, ...
+    const int ch = (int)(task / a.node_count);
+    const int ni = (int)(task - (int64_t)ch * a.node_count);
+    if (ch >= chunks) return;
     if (chunk_done<V>(a.done, ch)) return;
-    const int node = __ldg(a.order + a.node_begin + ni);
-    const int pos0 = __ldg(a.off + node);
     const int cw = ch * 32 * V + lane * V;
+    // one round of independent index loads (bucket-ordered flat tables)
+    const int32_t base = a.edge_begin + ni * D;
+    int slot[D];
+#pragma unroll
+    for (int i = 0; i < D; i++) slot[i] = __ldg(a.slot_ord + base + i);
 
     double b[D][V];
 #pragma unroll
@@ -84,9 +89,9 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
         double q[V];
         if constexpr (FROM_PRIOR) {
             // pre-pass (serial.py:58,166): q = p[v-bar] straight from the priors
-            load_v_cached<V>(a.P + (size_t)__ldg(a.idx + pos0 + i) * a.Bp + cw, q);
+            load_v_cached<V>(a.P + cofs(a.p_rows, __ldg(a.var_ord + base + i), cw), q);
         } else {
-            load_v<V>(a.msg + (size_t)(pos0 + i) * a.Bp + cw, q);
+            load_v<V>(a.msg + cofs(a.msg_rows, slot[i], cw), q);
         }
 #pragma unroll
         for (int v = 0; v < V; v++) b[i][v] = __dsub_rn(1.0, __dmul_rn(2.0, q[v]));
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
             for (int i = k + 1; i < D; i++) acc = __dmul_rn(acc, b[i][v]);
             out[v] = __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc)));
         }
-        store_v<V>(a.msg + (size_t)(pos0 + k) * a.Bp + cw, out);
+        store_v<V>(a.msg + cofs(a.msg_rows, slot[k], cw), out);
         if (k + 1 < D) {
 #pragma unroll
             for (int v = 0; v < V; v++) pre[v] = __dmul_rn(pre[v], b[k][v]);
@@ -120,10 +125,8 @@ __global__ void __launch_bounds__(kThreads) k_check_wide(NodeLaunch a, int TW, i
     extern __shared__ double sm[];
     double *b = sm;                         // [max_deg][TW]
     double *pre = sm + (size_t)max_deg * TW; // [max_deg][TW]
-    const int tiles = a.Bp / TW;
-    const int ni = blockIdx.x / tiles;
-    const int tile = blockIdx.x - ni * tiles;
-    if (ni >= a.node_count) return;
+    const int tile = blockIdx.x / a.node_count;  // tile-major: all nodes of tile 0 first
+    const int ni = blockIdx.x - tile * a.node_count;
     const int c = threadIdx.x % TW;
     const int worker = threadIdx.x / TW;
     const int nwk = blockDim.x / TW;
@@ -139,8 +142,8 @@ __global__ void __launch_bounds__(kThreads) k_check_wide(NodeLaunch a, int TW, i
     const int pos0 = __ldg(a.off + node);
     const int d = __ldg(a.off + node + 1) - pos0;
     for (int i = worker; i < d; i += nwk) {
-        double q = FROM_PRIOR ? __ldg(a.P + (size_t)__ldg(a.idx + pos0 + i) * a.Bp + cw)
-                              : __ldcs(a.msg + (size_t)(pos0 + i) * a.Bp + cw);
+        double q = FROM_PRIOR ? __ldg(a.P + cofs(a.p_rows, __ldg(a.idx + pos0 + i), cw))
+                              : __ldcs(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + i) : pos0 + i, cw));
         b[i * TW + c] = __dsub_rn(1.0, __dmul_rn(2.0, q));
     }
     __syncthreads();
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(kThreads) k_check_wide(NodeLaunch a, int TW, i
         const int k = (j & 1) ? (d - 1 - (j >> 1)) : (j >> 1);
         double acc = pre[k * TW + c];
         for (int i = k + 1; i < d; i++) acc = __dmul_rn(acc, b[i * TW + c]);
-        __stcs(a.msg + (size_t)(pos0 + k) * a.Bp + cw, __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc))));
+        __stcs(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + k) : pos0 + k, cw), __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc))));
     }
 }
 

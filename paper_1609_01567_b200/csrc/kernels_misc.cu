@@ -19,7 +19,7 @@ unsigned blocks_for(int64_t work, int threads, int64_t cap = 148 * 64) {
     return (unsigned)b;
 }
 
-// P_in [B][n] -> P [n][Bp]; padded codewords get p = 0.5 (no information).
+// P_in [B][n] -> P [Bp/64][n][64] (chunk-major); padded codewords get p = 0.5 (no information).
 __global__ void k_transpose_priors(const double *__restrict__ in, int32_t B, int32_t n, double *__restrict__ P,
                                    int32_t Bp) {
     __shared__ double tile[32][33];
@@ -31,7 +31,7 @@ __global__ void k_transpose_priors(const double *__restrict__ in, int32_t B, int
     __syncthreads();
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {
         const int j = j0 + y, c = c0 + threadIdx.x;
-        if (j < n && c < Bp) P[(size_t)j * Bp + c] = tile[threadIdx.x][y];
+        if (j < n && c < Bp) P[cofs(n, j, c)] = tile[threadIdx.x][y];
     }
 }
 
@@ -149,23 +149,25 @@ __global__ void k_count_errors(const uint32_t *est, int32_t RW, const uint8_t *s
 }
 
 // phase-API converters (not on the decode path) ------------------------------
-__global__ void k_canon_to_slots(const int32_t *chk_edge, int64_t E, const double *src, int32_t B, double *msg,
+__global__ void k_canon_to_slots(const int32_t *var_slot, int64_t E, const double *src, int32_t B, double *msg,
                                  int32_t Bp) {
     const int64_t total = E * Bp;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t pos = k / Bp;
-        const int c = (int)(k - pos * Bp);
-        msg[k] = (c < B) ? src[(size_t)c * E + chk_edge[pos]] : 0.5;
+        const int64_t e = k / Bp;
+        const int c = (int)(k - e * Bp);
+        const int32_t slot = var_slot ? var_slot[e] : (int32_t)e;
+        msg[cofs((int32_t)E, slot, c)] = (c < B) ? src[(size_t)c * E + e] : 0.5;
     }
 }
 
-__global__ void k_slots_to_canon(const int32_t *chk_edge, int64_t E, const double *msg, int32_t Bp, double *dst,
+__global__ void k_slots_to_canon(const int32_t *var_slot, int64_t E, const double *msg, int32_t Bp, double *dst,
                                  int32_t B) {
     const int64_t total = E * B;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t pos = k / B;
-        const int c = (int)(k - pos * B);
-        dst[(size_t)c * E + chk_edge[pos]] = msg[pos * Bp + c];
+        const int c = (int)(k / E);
+        const int64_t e = k - (int64_t)c * E;
+        const int32_t slot = var_slot ? var_slot[e] : (int32_t)e;
+        dst[k] = msg[cofs((int32_t)E, slot, c)];
     }
 }
 
@@ -246,14 +248,14 @@ int launch_count_errors(const uint32_t *est_bits, int32_t words_per_row, const u
 
 int launch_canon_to_slots(const ldpc_graph *g, const double *src, int32_t B, double *msg, int32_t Bp,
                           cudaStream_t s) {
-    k_canon_to_slots<<<blocks_for(g->E * Bp, 256), 256, 0, s>>>(g->chk_edge, g->E, src, B, msg, Bp);
+    k_canon_to_slots<<<blocks_for(g->E * Bp, 256), 256, 0, s>>>(g->var_slot, g->E, src, B, msg, Bp);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }
 
 int launch_slots_to_canon(const ldpc_graph *g, const double *msg, int32_t Bp, double *dst, int32_t B,
                           cudaStream_t s) {
-    k_slots_to_canon<<<blocks_for(g->E * B, 256), 256, 0, s>>>(g->chk_edge, g->E, msg, Bp, dst, B);
+    k_slots_to_canon<<<blocks_for(g->E * B, 256), 256, 0, s>>>(g->var_slot, g->E, msg, Bp, dst, B);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }
@@ -278,3 +280,76 @@ int launch_fill_u32(uint32_t *dst, uint32_t value, size_t count, cudaStream_t s)
 }
 
 }  // namespace ldpc
+
+// ---- self-test: ddiv_fast (when its test passes) == __ddiv_rn, bitwise ---------
+namespace ldpc {
+namespace {
+__device__ __forceinline__ uint64_t xs64(uint64_t &s) {
+    s ^= s << 13;
+    s ^= s >> 7;
+    s ^= s << 17;
+    return s;
+}
+
+__global__ void k_selftest_ddiv(uint64_t seed, int64_t count, unsigned long long *out) {
+    uint64_t s = seed ^ (0x9E3779B97F4A7C15ull * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1));
+    unsigned long long bad = 0, fast = 0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t u = xs64(s), v = xs64(s), w = xs64(s);
+        double a, b;
+        switch (w & 3) {
+            case 0: {  // decoder-like: q1 in [0,1], den = q0 + q1 in (0, 2]
+                a = (u >> 11) * 0x1.0p-53;
+                b = __dadd_rn(a, (v >> 11) * 0x1.0p-53);
+                break;
+            }
+            case 1: {  // products of messages: random exponents down to the subnormal range
+                a = __longlong_as_double((long long)((u & 0x000FFFFFFFFFFFFFull) | ((uint64_t)((w >> 8) % 1030) << 52)));
+                b = __dadd_rn(a, __longlong_as_double((long long)((v & 0x000FFFFFFFFFFFFFull) |
+                                                                  ((uint64_t)((w >> 20) % 1030) << 52))));
+                break;
+            }
+            case 2: {  // arbitrary positive finite bit patterns
+                a = __longlong_as_double((long long)(u & 0x7FEFFFFFFFFFFFFFull));
+                b = __longlong_as_double((long long)(v & 0x7FEFFFFFFFFFFFFFull));
+                break;
+            }
+            default: {  // mantissas near all-ones / powers of two
+                a = __longlong_as_double((long long)(0x3FE0000000000000ull | (u & 0xFull) | ((u >> 4 & 1) ? 0x000FFFFFFFFFFFF0ull : 0)));
+                b = __longlong_as_double((long long)(0x3FF0000000000000ull | (v & 0xFull) | ((v >> 4 & 1) ? 0x000FFFFFFFFFFFF0ull : 0)));
+                break;
+            }
+        }
+        bool ok;
+        const double q = ddiv_fast(a, b, ok);
+        if (ok) {
+            fast++;
+            if (__double_as_longlong(q) != __double_as_longlong(__ddiv_rn(a, b))) bad++;
+        }
+    }
+    atomicAdd(&out[0], bad);
+    atomicAdd(&out[1], fast);
+}
+}  // namespace
+}  // namespace ldpc
+
+extern "C" int ldpc_selftest_division(uint64_t seed, int64_t count, int64_t *result_host) {
+    using namespace ldpc;
+    LDPC_ARG_CHECK(result_host != nullptr && count > 0, "bad argument");
+    unsigned long long *d = nullptr;
+    LDPC_CUDA_TRY(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+    cudaMemset(d, 0, 2 * sizeof(unsigned long long));
+    k_selftest_ddiv<<<148 * 8, 256>>>(seed, count, d);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    unsigned long long h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) {
+        set_error("selftest: %s", cudaGetErrorString(e));
+        return LDPC_ECUDA;
+    }
+    result_host[0] = (int64_t)h[0];
+    result_host[1] = (int64_t)h[1];
+    return LDPC_OK;
+}

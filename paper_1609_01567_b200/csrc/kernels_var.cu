@@ -67,9 +67,10 @@ __global__ void __launch_bounds__(kThreads) k_var_reg(NodeLaunch a) {
     const int lane = threadIdx.x & 31;
     const int chunks = a.Bp / (32 * V);
     const int64_t task = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    const int ni = (int)(task / chunks);
-    const int ch = (int)(task - (int64_t)ni * chunks);
-    if (ni >= a.node_count) return;
+    // chunk-major sweep: all nodes of codeword chunk 0, then chunk 1, ...
+    const int ch = (int)(task / a.node_count);
+    const int ni = (int)(task - (int64_t)ch * a.node_count);
+    if (ch >= chunks) return;
     if (a.done != nullptr) {
         bool all;
         if constexpr (V == 2) {
@@ -80,19 +81,19 @@ __global__ void __launch_bounds__(kThreads) k_var_reg(NodeLaunch a) {
         }
         if (all) return;
     }
-    const int node = __ldg(a.order + a.node_begin + ni);
-    const int e0 = __ldg(a.off + node);
     const int cw = ch * 32 * V + lane * V;
+    // one round of independent index loads (bucket-ordered flat tables)
+    const int node = __ldg(a.order + a.node_begin + ni);
+    const int32_t base = a.edge_begin + ni * D;
+    int pos[D];
+#pragma unroll
+    for (int i = 0; i < D; i++) pos[i] = __ldg(a.slot_ord + base + i);
 
     double pj[V];
-    load_prior<V>(a.P + (size_t)node * a.Bp + cw, pj);
-    int pos[D];
+    load_prior<V>(a.P + cofs(a.p_rows, node, cw), pj);
     double r[D][V];
 #pragma unroll
-    for (int i = 0; i < D; i++) {
-        pos[i] = __ldg(a.idx + e0 + i);
-        load_v<V>(a.msg + (size_t)pos[i] * a.Bp + cw, r[i]);
-    }
+    for (int i = 0; i < D; i++) load_v<V>(a.msg + cofs(a.msg_rows, pos[i], cw), r[i]);
     double om[D][V];  // 1 - r_i
 #pragma unroll
     for (int i = 0; i < D; i++)
@@ -105,10 +106,12 @@ __global__ void __launch_bounds__(kThreads) k_var_reg(NodeLaunch a) {
         pre0[v] = __dsub_rn(1.0, pj[v]);
         pre1[v] = pj[v];
     }
+    uint32_t slow = 0;  // outputs whose division needs the library slow path (or den == 0)
 #pragma unroll
     for (int k = 0; k < D; k++) {
         if constexpr (WRITE_Q) {
             double out[V];
+            bool all_ok = true;
 #pragma unroll
             for (int v = 0; v < V; v++) {
                 double q0 = pre0[v], q1 = pre1[v];
@@ -117,15 +120,37 @@ __global__ void __launch_bounds__(kThreads) k_var_reg(NodeLaunch a) {
                     q0 = __dmul_rn(q0, om[i][v]);
                     q1 = __dmul_rn(q1, r[i][v]);
                 }
-                const double den = __dadd_rn(q0, q1);
-                out[v] = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
+                bool ok;
+                out[v] = ddiv_fast(q1, __dadd_rn(q0, q1), ok);  // den == 0 -> !ok
+                all_ok = all_ok && ok;
             }
-            store_v<V>(a.msg + (size_t)pos[k] * a.Bp + cw, out);
+            if (all_ok) store_v<V>(a.msg + cofs(a.msg_rows, pos[k], cw), out);
+            else slow |= 1u << k;
         }
 #pragma unroll
         for (int v = 0; v < V; v++) {
             pre0[v] = __dmul_rn(pre0[v], om[k][v]);
             pre1[v] = __dmul_rn(pre1[v], r[k][v]);
+        }
+    }
+    if constexpr (WRITE_Q) {
+        if (slow) {  // rare: tiny/zero denominators; recompute in reference order, divide via the library
+            for (int k = 0; k < D; k++) {
+                if (!((slow >> k) & 1u)) continue;
+                double out[V];
+#pragma unroll
+                for (int v = 0; v < V; v++) {
+                    double q0 = __dsub_rn(1.0, pj[v]), q1 = pj[v];
+                    for (int i = 0; i < D; i++) {
+                        if (i == k) continue;
+                        q0 = __dmul_rn(q0, om[i][v]);
+                        q1 = __dmul_rn(q1, r[i][v]);
+                    }
+                    const double den = __dadd_rn(q0, q1);
+                    out[v] = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
+                }
+                store_v<V>(a.msg + cofs(a.msg_rows, pos[k], cw), out);
+            }
         }
     }
     // estimate: c_hat = 0 iff Q0 > Q1 (ties -> 1), serial.py:132
@@ -153,10 +178,8 @@ __global__ void __launch_bounds__(kThreads) k_var_wide(NodeLaunch a, int TW, int
     double *pre0 = r + (size_t)max_deg * TW;         // [max_deg+1][TW]
     double *pre1 = pre0 + (size_t)(max_deg + 1) * TW; // [max_deg+1][TW]
     int *spos = reinterpret_cast<int *>(pre1 + (size_t)(max_deg + 1) * TW);  // [max_deg]
-    const int tiles = a.Bp / TW;
-    const int ni = blockIdx.x / tiles;
-    const int tile = blockIdx.x - ni * tiles;
-    if (ni >= a.node_count) return;
+    const int tile = blockIdx.x / a.node_count;  // tile-major: all nodes of tile 0 first
+    const int ni = blockIdx.x - tile * a.node_count;
     const int c = threadIdx.x % TW;
     const int worker = threadIdx.x / TW;
     const int nwk = blockDim.x / TW;
@@ -167,12 +190,12 @@ __global__ void __launch_bounds__(kThreads) k_var_wide(NodeLaunch a, int TW, int
     const int node = __ldg(a.order + a.node_begin + ni);
     const int e0 = __ldg(a.off + node);
     const int d = __ldg(a.off + node + 1) - e0;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) spos[i] = __ldg(a.idx + e0 + i);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) spos[i] = a.slot ? __ldg(a.slot + e0 + i) : e0 + i;
     __syncthreads();
-    for (int i = worker; i < d; i += nwk) r[i * TW + c] = __ldcs(a.msg + (size_t)spos[i] * a.Bp + cw);
+    for (int i = worker; i < d; i += nwk) r[i * TW + c] = __ldcs(a.msg + cofs(a.msg_rows, spos[i], cw));
     __syncthreads();
     if (worker == 0) {
-        const double p = __ldg(a.P + (size_t)node * a.Bp + cw);
+        const double p = __ldg(a.P + cofs(a.p_rows, node, cw));
         double x0 = __dsub_rn(1.0, p), x1 = p;
         for (int i = 0; i < d; i++) {
             pre0[i * TW + c] = x0;
@@ -195,7 +218,10 @@ __global__ void __launch_bounds__(kThreads) k_var_wide(NodeLaunch a, int TW, int
                 q1 = __dmul_rn(q1, ri);
             }
             const double den = __dadd_rn(q0, q1);
-            __stcs(a.msg + (size_t)spos[k] * a.Bp + cw, (den == 0.0) ? 0.5 : __ddiv_rn(q1, den));
+            bool ok;
+            double q = ddiv_fast(q1, den, ok);
+            if (!ok) q = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
+            __stcs(a.msg + cofs(a.msg_rows, spos[k], cw), q);
         }
     }
     if (worker == 0) {

@@ -163,3 +163,15 @@ class TestSyndrome:
     def test_length_mismatch(self, tables14):
         with pytest.raises(ValueError):
             syndrome(np.zeros(13, dtype=np.uint8), tables14)
+
+
+def test_fast_division_is_bitwise_ddiv_rn(cuda):
+    """The branch-free division path (common.cuh ddiv_fast) equals __ddiv_rn bit for bit."""
+    from paper_1609_01567_b200 import _native
+
+    res = np.zeros(2, dtype=np.int64)
+    for seed in (1, 2, 3, 4):
+        rc = _native.lib().ldpc_selftest_division(seed, 1 << 28, res.ctypes.data_as(_native.P_i64))
+        _native.check(rc, "selftest")
+        assert res[0] == 0, f"{res[0]} mismatches"
+        assert res[1] > (1 << 26)
