@@ -25,13 +25,20 @@ namespace {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 }  // namespace
 
-// LDPC_KERNEL=pipe selects the bulk-copy ring kernels (A/B comparisons); default: register loads
-bool use_pipe_kernels() {
-    static const bool pipe = [] {
+// Kernel family per (side, degree) for the register-path degrees (<= kMaxRegDegree):
+// the cp.async ring (kernels_pipe.cu) or register loads (kernels_check/var.cu).
+// Measured on B200 (profiles/r1_kernel_choice.md): the ring wins for variable
+// nodes of degree >= 3, register loads for degree-2 variables and for checks.
+// LDPC_KERNEL=reg|pipe forces one family (A/B runs).
+bool use_ring(bool var_side, int deg) {
+    static const int forced = [] {
         const char *e = getenv("LDPC_KERNEL");
-        return e && std::string(e) == "pipe";
+        if (e && std::string(e) == "reg") return 1;
+        if (e && std::string(e) == "pipe") return 2;
+        return 0;
     }();
-    return pipe;
+    if (forced) return forced == 2;
+    return var_side && deg >= 3;
 }
 
 size_t workspace_bytes(const ldpc_graph *g, int32_t B) {
@@ -149,7 +156,7 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
-            int rc = use_pipe_kernels() ? launch_check_pipe(a, b.deg, from_prior, s)
+            int rc = use_ring(false, b.deg) ? launch_check_pipe(a, b.deg, from_prior, s)
                                         : launch_check_bucket(a, b.deg, from_prior, s);
             if (rc) return rc;
         } else {
@@ -174,7 +181,7 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
-            int rc = use_pipe_kernels() ? launch_var_pipe(a, b.deg, write_q, s)
+            int rc = use_ring(true, b.deg) ? launch_var_pipe(a, b.deg, write_q, s)
                                         : launch_var_bucket(a, b.deg, write_q, s);
             if (rc) return rc;
         } else {

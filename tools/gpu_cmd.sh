@@ -1,3 +1,4 @@
-python tools/membench.py > gpurun_out/membench.json 2>&1; cat gpurun_out/membench.json
-LDPC_SLOTS=var timeout 600 python -m pytest tests -q -m gpu --timeout 600 -p no:cacheprovider -x 2>&1 | tail -2
-EXTRA_VARIANTS="LDPC_SLOTS=var LDPC_KERNEL=pipe,LDPC_SLOTS=var" bash profiles/variants.sh
+LDPC_KERNEL=pipe timeout 600 python -m pytest tests -q -m gpu --timeout 600 -p no:cacheprovider -x > gpurun_out/pytest_pipe.log 2>&1; tail -1 gpurun_out/pytest_pipe.log
+for k in reg pipe; do
+LDPC_KERNEL=$k timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(check|var|node)" -c 40 --csv --log-file gpurun_out/launches_$k.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > /dev/null 2>&1
+done
