@@ -1,4 +1,4 @@
-LDPC_KERNEL=pipe timeout 600 python -m pytest tests -q -m gpu --timeout 600 -p no:cacheprovider -x > gpurun_out/pytest_pipe.log 2>&1; tail -1 gpurun_out/pytest_pipe.log
-for k in reg pipe; do
-LDPC_KERNEL=$k timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(check|var|node)" -c 40 --csv --log-file gpurun_out/launches_$k.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > /dev/null 2>&1
-done
+timeout 900 python bench.py > gpurun_out/bench_r1.json 2> gpurun_out/bench_r1.err; echo bench_rc=$?
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_r1.json 2>&1
+bash profiles/ncu_capture.sh r1c
+python tools/ncu_traffic.py gpurun_out/prof_r1c_var.ncu-rep gpurun_out/prof_r1c_check.ncu-rep gpurun_out/ncu_traffic.json

@@ -36,15 +36,17 @@ def report(path):
         d = dict(zip(hdr, r))
         name = re.sub(r"\(.*", "", d.get("Kernel Name", "?")).replace("void ", "").replace("(anonymous namespace)::", "")
         e = {"kernel": name.strip(), "grid": d.get("Grid Size"), "block": d.get("Block Size")}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
         for m, u, sc in METRICS:
             if m in d and d[m] not in ("", "n/a"):
                 try:
-                    e[m] = round(float(d[m].replace(",", "")) * (sc if units[hdr.index(m)] not in ("%",) else 1), 3)
+                    v = float(d[m].replace(",", ""))
+                    unit = units[hdr.index(m)]
+                    if unit in scale:  # normalise to bytes -> MB, time -> us
+                        v = v * scale[unit] * (1e-6 if "byte" in unit else 1)
+                    e[m] = round(v, 3)
                 except ValueError:
                     pass
-        if "dram__bytes_read.sum" in e:
-            # units from ncu are bytes-scaled already (Mbyte/Gbyte); recompute from raw bytes when possible
-            pass
         res.append(e)
     return res
 
