@@ -1,0 +1,255 @@
+"""AWGN channel, frame seeding and the BER sweep, sharded over GPUs.
+
+Mirrors the reference's channel/RNG layer (edgeldpc/rng.py:34-80,
+channel.py:31-148): xorshift128+ with per-frame states derived from
+(seed, point, frame), BPSK 0 -> -1 over AWGN via Box-Muller, and ber_sweep's
+fold of (bit errors, iterations, failures) in frame order.
+
+Multi-GPU: frames of every Eb/N0 point are split into
+contiguous per-rank ranges; each rank decodes its own frames on its own GPU
+and the only collective is one allreduce of int64[4] = {bit errors, failures,
+iterations, frames} per point.  Integer sums are exact, so the BerPoints are
+identical for any number of ranks (and to the single-process reference).
+
+Channel arithmetic: the integer RNG is exact.  ``exact_channel=True`` runs
+Box-Muller with Python's math functions element by element, exactly like
+channel.py:31-37, so y -- and with the bit-exact decoder the whole BerPoint --
+equals the reference's.  The default vectorised path uses numpy's log/cos/sin,
+which may differ from libm in the last ulp (statistically identical noise, not
+bit-identical; the reference's channel arithmetic is itself untested).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+MASK64 = (1 << 64) - 1
+_GOLDEN = 0x9E3779B97F4A7C15
+DEFAULT_BATCH = 1024
+
+
+# ---- rng.py:34-80 -------------------------------------------------------------
+
+@dataclass(frozen=True)
+class RngState:
+    s0: int
+    s1: int
+
+    def __post_init__(self):
+        if not (0 <= self.s0 <= MASK64 and 0 <= self.s1 <= MASK64):
+            raise ValueError("state words must be unsigned 64-bit integers")
+        if self.s0 == 0 and self.s1 == 0:
+            raise ValueError("all-zero state is a fixed point of xorshift128+")
+
+
+def rng_next(state: RngState) -> tuple[RngState, int]:
+    """xorshift128+ (23/18/5), rng.py:34-41."""
+    x, y = state.s0, state.s1
+    x ^= (x << 23) & MASK64
+    x ^= x >> 18
+    x ^= y ^ (y >> 5)
+    return RngState(y, x), (x + y) & MASK64
+
+
+def u01_from_bits(x: int) -> float:
+    """Top 53 bits + 1, scaled by 2^-53: a double in (0, 1] (rng.py:44-50)."""
+    return ((x >> 11) + 1) * 2.0**-53
+
+
+def rng_uniform01(state: RngState) -> tuple[RngState, float]:
+    state, x = rng_next(state)
+    return state, u01_from_bits(x)
+
+
+def _mix64(z: int) -> int:
+    z &= MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return z ^ (z >> 31)
+
+
+def derive_state(*keys: int) -> RngState:
+    """splitmix64-style per-frame state (rng.py:67-80)."""
+    acc = 0
+    for k in keys:
+        acc = _mix64((acc + _GOLDEN + (k & MASK64)) & MASK64)
+    s0 = _mix64((acc + _GOLDEN) & MASK64)
+    s1 = _mix64((acc + 2 * _GOLDEN) & MASK64)
+    if s0 == 0 and s1 == 0:
+        s1 = _GOLDEN
+    return RngState(s0, s1)
+
+
+# ---- channel.py:31-67 -------------------------------------------------------
+
+def box_muller(u1: float, u2: float) -> tuple[float, float]:
+    """Standard normal pair from two uniforms, u1 in (0, 1] (channel.py:31-37)."""
+    if u1 <= 0.0:
+        raise ValueError("u1 must be positive")
+    radius = math.sqrt(-2.0 * math.log(u1))
+    angle = 2.0 * math.pi * u2
+    return radius * math.cos(angle), radius * math.sin(angle)
+
+
+def ebno_to_sigma2(ebno_db: float, rate: float) -> float:
+    """channel.py:40-44."""
+    if not 0.0 < rate < 1.0:
+        raise ValueError("rate must be in (0, 1)")
+    return 1.0 / (2.0 * rate * 10.0 ** (ebno_db / 10.0))
+
+
+def transmit_all_zero(n: int, sigma2: float, state: RngState) -> tuple[RngState, np.ndarray]:
+    """y_j = -1 + sigma z_j, pairs of uniforms per normal pair (channel.py:47-67)."""
+    if sigma2 <= 0.0:
+        raise ValueError("sigma2 must be positive")
+    sigma = math.sqrt(sigma2)
+    y = np.empty(n)
+    i = 0
+    while i < n:
+        state, u1 = rng_uniform01(state)
+        state, u2 = rng_uniform01(state)
+        z0, z1 = box_muller(u1, u2)
+        y[i] = -1.0 + sigma * z0
+        i += 1
+        if i < n:
+            y[i] = -1.0 + sigma * z1
+            i += 1
+    return state, y
+
+
+def uniforms_batch(states: list[RngState], count: int) -> np.ndarray:
+    """[F, count] uniforms of F independent xorshift128+ streams, integer-exact, vectorised over frames."""
+    s0 = np.array([s.s0 for s in states], dtype=np.uint64)
+    s1 = np.array([s.s1 for s in states], dtype=np.uint64)
+    out = np.empty((len(states), count), dtype=np.float64)
+    scale = np.float64(2.0**-53)
+    with np.errstate(over="ignore"):
+        for k in range(count):
+            x, y = s0, s1
+            x = x ^ (x << np.uint64(23))
+            x = x ^ (x >> np.uint64(18))
+            x = x ^ (y ^ (y >> np.uint64(5)))
+            s0, s1 = y, x
+            out[:, k] = (((x + y) >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * scale
+    return out
+
+
+def transmit_all_zero_batch(n: int, sigma2: float, states: list[RngState], exact: bool = False) -> np.ndarray:
+    """Received frames [F, n] for the all-zero codeword, one seeded stream per frame."""
+    if sigma2 <= 0.0:
+        raise ValueError("sigma2 must be positive")
+    if exact:
+        return np.stack([transmit_all_zero(n, sigma2, s)[1] for s in states]) if states else np.empty((0, n))
+    pairs = (n + 1) // 2
+    u = uniforms_batch(states, 2 * pairs)
+    u1, u2 = u[:, 0::2], u[:, 1::2]
+    radius = np.sqrt(-2.0 * np.log(u1))
+    angle = 2.0 * math.pi * u2
+    z = np.empty((len(states), 2 * pairs))
+    z[:, 0::2] = radius * np.cos(angle)
+    z[:, 1::2] = radius * np.sin(angle)
+    return -1.0 + math.sqrt(sigma2) * z[:, :n]
+
+
+# ---- channel.py:70-148 ------------------------------------------------------
+
+@dataclass(frozen=True)
+class BerPoint:
+    ebno_db: float
+    sigma2: float
+    frames: int
+    bit_errors: int
+    ber: float
+    mean_iterations: float
+    failures: int
+
+
+def shard_range(frames: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous frame range of one rank (frames [lo, hi))."""
+    return frames * rank // world, frames * (rank + 1) // world
+
+
+def _dist_info():
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return dist, dist.get_rank(), dist.get_world_size()
+    except Exception:
+        pass
+    return None, 0, 1
+
+
+def gpu_decode_counts(decoder):
+    """decode_fn for ber_sweep: GPU decode of a batch, error counts accumulated on the device."""
+    import torch
+
+    from .decoder import priors_awgn_batch
+
+    def run(Y, sigma2, max_iterations, counts):
+        P = torch.from_numpy(priors_awgn_batch(Y, sigma2)).to(counts.device)
+        outs = decoder.decode_device(P, max_iterations, early_stop=True, syndrome_out=False)
+        decoder.count_errors(outs, counts)
+
+    return run
+
+
+def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int = 0,
+              batch: int = DEFAULT_BATCH, rate: float | None = None, decode_fn=None,
+              exact_channel: bool = False, device=None) -> list[BerPoint]:
+    """channel.py:83-137 on the GPU, frames sharded over torch.distributed ranks.
+
+    decode_fn(Y [b, n], sigma2, max_iterations, counts) must add
+    [bit errors, failures, iterations, frames] of the batch into the int64[4]
+    tensor ``counts``; the default decodes on this rank's GPU.
+    """
+    import torch
+
+    if frames < 1:
+        raise ValueError("frames must be at least 1")
+    if batch < 1:
+        raise ValueError("batch must be at least 1")
+    dist, rank, world = _dist_info()
+    R = rate if rate is not None else (H.n - H.m) / H.n
+    decoder = None
+    if decode_fn is None:
+        from .decoder import ParallelDecoder
+        from .tables import CodeTables
+
+        decoder = ParallelDecoder(CodeTables.from_matrix(H), max_batch=batch)
+        decode_fn = gpu_decode_counts(decoder)
+        device = device or torch.device("cuda", torch.cuda.current_device())
+    device = device or torch.device("cpu")
+    lo, hi = shard_range(frames, rank, world)
+    points = []
+    try:
+        for index, ebno_db in enumerate(ebno_points):
+            sigma2 = ebno_to_sigma2(float(ebno_db), R)
+            counts = torch.zeros(4, dtype=torch.int64, device=device)
+            for b0 in range(lo, hi, batch):
+                fr = range(b0, min(hi, b0 + batch))
+                states = [derive_state(seed, index, f) for f in fr]   # channel.py:112
+                Y = transmit_all_zero_batch(H.n, sigma2, states, exact=exact_channel)
+                decode_fn(Y, sigma2, max_iterations, counts)
+            if dist is not None:
+                dist.all_reduce(counts)                                # the only collective
+            c = [int(x) for x in counts.cpu().tolist()]
+            assert c[3] == frames, "frame count mismatch after the allreduce"
+            points.append(BerPoint(ebno_db=float(ebno_db), sigma2=sigma2, frames=frames, bit_errors=c[0],
+                                   ber=c[0] / (frames * H.n), mean_iterations=c[2] / frames, failures=c[1]))
+    finally:
+        if decoder is not None:
+            decoder.close()
+    return points
+
+
+def ber_csv(points: list[BerPoint]) -> str:
+    """channel.py:140-148: full-precision (round-trip) floats."""
+    lines = ["ebno_db,sigma2,frames,bit_errors,ber,mean_iterations,failures"]
+    for pt in points:
+        lines.append(f"{pt.ebno_db!r},{pt.sigma2!r},{pt.frames},{pt.bit_errors},"
+                     f"{pt.ber!r},{pt.mean_iterations!r},{pt.failures}")
+    return "\n".join(lines) + "\n"

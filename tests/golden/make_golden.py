@@ -16,6 +16,8 @@ Contents:
   decode.npz   priors (reference priors_awgn, i.e. numpy exp on this machine),
                decode_awgn results, and a fixed-iteration run composed from the
                reference's exported phase functions (no early exit).
+  channel.npz  xorshift128+ / derive_state KATs, exact received frames and the
+               reference ber_sweep points + CSV for the (96,48) and (14,7) codes.
 """
 
 from __future__ import annotations
@@ -167,10 +169,36 @@ def save_decode(cs: dict) -> None:
     np.savez_compressed(HERE / "decode.npz", **d)
 
 
+def save_channel(cs: dict) -> None:
+    """rng.py / channel.py outputs: RNG KATs, exact received frames, reference ber_sweep points."""
+    d = {}
+    st = ref.RngState(1, 2)
+    outs = []
+    for _ in range(64):
+        st, x = ref.rng_next(st)
+        outs.append(x)
+    d["rng/outputs_1_2"] = np.array(outs, dtype=np.uint64)
+    keys = [(0, 0, 0), (5, 1, 7), (2**40 + 3, 2, 11)]
+    d["rng/derive_keys"] = np.array(keys, dtype=np.uint64)
+    d["rng/derive_states"] = np.array([[ref.derive_state(*k).s0, ref.derive_state(*k).s1] for k in keys], dtype=np.uint64)
+    Y = np.stack([ref.transmit_all_zero(96, 0.63, ref.derive_state(5, 0, f))[1] for f in range(6)])
+    d["channel/y_h96_seed5"] = Y
+    for name, code, pts, frames, it, seed in (("h96", "h96", (1.0, 2.0, 3.0), 24, 20, 5),
+                                             ("h14", "h14", (0.0, 2.0), 16, 10, 9)):
+        P = ref.ber_sweep(cs[code], pts, frames, max_iterations=it, seed=seed, decoders_in_flight=1)
+        d[f"ber/{name}/args"] = np.array([frames, it, seed])
+        d[f"ber/{name}/ebno"] = np.array(pts)
+        d[f"ber/{name}/points"] = np.array([[p.ebno_db, p.sigma2, p.frames, p.bit_errors, p.ber, p.mean_iterations,
+                                              p.failures] for p in P])
+        d[f"ber/{name}/csv"] = np.array(ref.ber_csv(P))
+    np.savez_compressed(HERE / "channel.npz", **d)
+
+
 if __name__ == "__main__":
     cs = codes()
     save_tables(cs)
     save_phases(cs)
     save_decode(cs)
+    save_channel(cs)
     for f in sorted(HERE.glob("*.npz")):
         print(f.name, f.stat().st_size, "bytes")

@@ -194,3 +194,18 @@ def test_dvbs2_full_batch(cuda):
     assert np.array_equal(res2.estimates()[sample], e2)
     assert np.array_equal(res2.iterations[sample], it2)
     assert np.array_equal(res2.success[sample].astype(bool), ok2)
+
+
+@pytest.mark.parametrize("name", ["h96", "h14"])
+def test_ber_sweep_gpu_matches_reference(cuda, golden_tables, name):
+    """channel.py:83-137 semantics on the GPU decoder: BerPoints and CSV equal the reference's."""
+    from conftest import GOLDEN
+    from paper_1609_01567_b200 import channel as ch
+
+    g = np.load(GOLDEN / "channel.npz")
+    H = golden_code(golden_tables, name)
+    frames, it, seed = (int(x) for x in g[f"ber/{name}/args"])
+    pts = ch.ber_sweep(H, g[f"ber/{name}/ebno"], frames, max_iterations=it, seed=seed, batch=8, exact_channel=True)
+    arr = np.array([[p.ebno_db, p.sigma2, p.frames, p.bit_errors, p.ber, p.mean_iterations, p.failures] for p in pts])
+    assert np.array_equal(arr, g[f"ber/{name}/points"])
+    assert ch.ber_csv(pts) == str(g[f"ber/{name}/csv"])
