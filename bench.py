@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--sub-batch", type=int, default=0, help="e2e pipeline sub-batch (0 = decoder default)")
     return ap.parse_args()
 
 
@@ -230,7 +231,7 @@ def run_ours(args):
     B = args.batch or C["batch"]
     iters = args.iters if args.iters is not None else C["max_iterations"]
     T = CodeTables.from_matrix(H)
-    dec = ParallelDecoder(T, max_batch=B)
+    dec = ParallelDecoder(T, max_batch=B, sub_batch=args.sub_batch)
     P_host, _ = synthetic_priors(H, B, args.ebno, seed=1000 + rank)
     P_pin = torch.from_numpy(P_host).pin_memory()
     P_dev = P_pin.to(dev, non_blocking=True)

@@ -25,6 +25,15 @@ namespace {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 }  // namespace
 
+// LDPC_GRAPHS=0 disables CUDA-graph replay of decode sequences
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LDPC_GRAPHS");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
 // Kernel family per (side, degree) for the register-path degrees (<= kMaxRegDegree):
 // the cp.async ring (kernels_pipe.cu) or register loads (kernels_check/var.cu).
 // Measured on B200 (profiles/r1_kernel_choice.md): the ring wins for variable
@@ -266,16 +275,68 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
+    auto sequence = [&](Prof &prof) -> int {
+        const int64_t n = g->n, m = g->m;
+        RUN(LDPC_KCLASS_LAYOUT, 16 * n * B, launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s));
+        int r = run_decode(g, w, max_iterations, early, s, prof);
+        if (r) return r;
+        RUN(LDPC_KCLASS_LAYOUT, (n / 8) * 2 * B, launch_pack_rows(w.chat, g->n, w.NW, B, est_bits_dev, s));
+        if (syn_bits_dev)
+            RUN(LDPC_KCLASS_LAYOUT, (m / 8) * 2 * B, launch_pack_rows(w.zb, g->m, w.NW, B, syn_bits_dev, s));
+        RUN(LDPC_KCLASS_LAYOUT, 0, launch_finalize(w, early, max_iterations, success_dev, iters_dev, s));
+        return LDPC_OK;
+    };
     Prof prof;
     prof.out = prof_host;
     prof.s = s;
-    const int64_t n = g->n, m = g->m;
-    RUN(LDPC_KCLASS_LAYOUT, 16 * n * B, launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s));
-    rc = run_decode(g, w, max_iterations, early, s, prof);
+    if (prof_host == nullptr && s != nullptr && graphs_enabled()) {
+        // Replay the whole sequence (~50 dependent launches at C3) as one CUDA
+        // graph: captured on the second call with the same pointers and sizes
+        // (the first call runs eagerly and initialises every launcher), then
+        // launched from the cache.
+        auto *gg = const_cast<ldpc_graph *>(g);
+        const ldpc_graph::GraphKey key{p_dev, B, max_iterations, flags, est_bits_dev, success_dev, iters_dev,
+                                       syn_bits_dev, workspace_dev, stream};
+        ldpc_graph::GraphEntry *entry;
+        {
+            std::lock_guard<std::mutex> lock(gg->graphs_mu);
+            entry = &gg->graphs[key];
+            entry->uses++;
+        }
+        if (entry->exec == nullptr && entry->uses >= 2) {
+            cudaGraph_t graph = nullptr;
+            const long long k0 = ldpc_kernel_launches();
+            LDPC_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            int r = sequence(prof);
+            cudaError_t ce = cudaStreamEndCapture(s, &graph);
+            const long long kernels = ldpc_kernel_launches() - k0;
+            count_launches(-kernels);  // captured, not executed
+            if (r != LDPC_OK || ce != cudaSuccess || graph == nullptr) {
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();
+                if (r != LDPC_OK) return r;
+                set_error("graph capture: %s", cudaGetErrorString(ce));
+                return LDPC_ECUDA;
+            }
+            cudaGraphExec_t exec = nullptr;
+            ce = cudaGraphInstantiate(&exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ce != cudaSuccess) {
+                set_error("graph instantiate: %s", cudaGetErrorString(ce));
+                return LDPC_ECUDA;
+            }
+            std::lock_guard<std::mutex> lock(gg->graphs_mu);
+            entry->exec = exec;
+            entry->kernels = kernels;
+        }
+        if (entry->exec != nullptr) {
+            LDPC_CUDA_TRY(cudaGraphLaunch(entry->exec, s));
+            count_launches(entry->kernels);
+            return LDPC_OK;
+        }
+    }
+    rc = sequence(prof);
     if (rc) return rc;
-    RUN(LDPC_KCLASS_LAYOUT, (n / 8) * 2 * B, launch_pack_rows(w.chat, g->n, w.NW, B, est_bits_dev, s));
-    if (syn_bits_dev) RUN(LDPC_KCLASS_LAYOUT, (m / 8) * 2 * B, launch_pack_rows(w.zb, g->m, w.NW, B, syn_bits_dev, s));
-    RUN(LDPC_KCLASS_LAYOUT, 0, launch_finalize(w, early, max_iterations, success_dev, iters_dev, s));
     return prof.flush();
 }
 
@@ -339,35 +400,65 @@ extern "C" int ldpc_phase_syndrome(const ldpc_graph *g, const uint8_t *chat_dev,
     return launch_bits_to_bytes(w.zb, g->m, w.NW, B, z_dev, s);
 }
 
-// ---- host-buffer decoder: pipelined H2D / decode / D2H over two streams -------
+// ---- host-buffer decoder: pipelined H2D / decode / D2H ------------------------
+// Device input and output buffers cover the whole max_batch, so every
+// sub-batch's H2D copy is enqueued up front on the copy stream (one event per
+// sub-batch) before the host spends time enqueuing decode launches; the compute
+// stream waits per sub-batch and the output stream returns each sub-batch's
+// packed results as soon as it is decoded.  Sub-batches grow geometrically
+// (64, 96, 144, ... up to `sub`) so the pipeline fill -- the first H2D, which
+// nothing overlaps -- stays short while later sub-batches are large enough to
+// run the kernels efficiently.
+namespace {
+constexpr int kMaxChunks = 64;
+}
+
 struct ldpc_decoder {
     const ldpc_graph *g = nullptr;
     int32_t max_batch = 0, sub = 0;
-    cudaStream_t st[2] = {nullptr, nullptr};
-    void *ws[2] = {nullptr, nullptr};
+    cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+    void *ws = nullptr;  // one workspace: decodes are serialised on s_comp
     size_t ws_bytes = 0;
-    double *p[2] = {nullptr, nullptr};
-    uint32_t *est[2] = {nullptr, nullptr};
-    uint32_t *syn[2] = {nullptr, nullptr};
-    uint8_t *succ[2] = {nullptr, nullptr};
-    int32_t *its[2] = {nullptr, nullptr};
+    double *p = nullptr;      // [max_batch][n]
+    uint32_t *est = nullptr;  // [max_batch][RWn]
+    uint32_t *syn = nullptr;  // [max_batch][RWm]
+    uint8_t *succ = nullptr;  // [max_batch]
+    int32_t *its = nullptr;   // [max_batch]
+    cudaEvent_t in_ready[kMaxChunks] = {}, decoded[kMaxChunks] = {};
     bool poisoned = false;
     std::mutex mu;
 };
 
 static void decoder_free(ldpc_decoder *d) {
     if (!d) return;
-    for (int i = 0; i < 2; i++) {
-        if (d->st[i]) cudaStreamSynchronize(d->st[i]);
-        cudaFree(d->ws[i]);
-        cudaFree(d->p[i]);
-        cudaFree(d->est[i]);
-        cudaFree(d->syn[i]);
-        cudaFree(d->succ[i]);
-        cudaFree(d->its[i]);
-        if (d->st[i]) cudaStreamDestroy(d->st[i]);
-    }
+    for (cudaStream_t s : {d->s_in, d->s_comp, d->s_out})
+        if (s) cudaStreamSynchronize(s);
+    cudaFree(d->ws);
+    cudaFree(d->p);
+    cudaFree(d->est);
+    cudaFree(d->syn);
+    cudaFree(d->succ);
+    cudaFree(d->its);
+    for (int i = 0; i < kMaxChunks; i++)
+        for (cudaEvent_t e : {d->in_ready[i], d->decoded[i]})
+            if (e) cudaEventDestroy(e);
+    for (cudaStream_t s : {d->s_in, d->s_comp, d->s_out})
+        if (s) cudaStreamDestroy(s);
     delete d;
+}
+
+// sub-batch sizes for a batch of B: 64, 96, 144, ... capped at sub, the last one takes the rest
+static std::vector<int32_t> chunk_plan(int32_t B, int32_t sub) {
+    std::vector<int32_t> v;
+    int32_t b = std::min<int32_t>(sub, 64);
+    for (int32_t c0 = 0; c0 < B;) {
+        int32_t take = std::min(b, B - c0);
+        if ((int)v.size() == kMaxChunks - 1) take = B - c0;  // keep within the event budget
+        v.push_back(take);
+        c0 += take;
+        b = std::min<int32_t>(sub, std::max<int32_t>(b, (b * 3 / 2) / 32 * 32));
+    }
+    return v;
 }
 
 extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32_t sub_batch, ldpc_decoder **out) {
@@ -377,22 +468,28 @@ extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32
     ldpc_decoder *d = new ldpc_decoder();
     d->g = g;
     d->max_batch = max_batch;
-    d->sub = sub_batch > 0 ? std::min(sub_batch, max_batch) : std::min(max_batch, 256);
-    d->ws_bytes = workspace_bytes(g, d->sub);
-    const size_t RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32;
-    for (int i = 0; i < 2; i++) {
-        cudaError_t e = cudaStreamCreateWithFlags(&d->st[i], cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaMalloc(&d->ws[i], d->ws_bytes);
-        if (e == cudaSuccess) e = cudaMalloc((void **)&d->p[i], sizeof(double) * (size_t)g->n * d->sub);
-        if (e == cudaSuccess) e = cudaMalloc((void **)&d->est[i], sizeof(uint32_t) * RWn * d->sub);
-        if (e == cudaSuccess) e = cudaMalloc((void **)&d->syn[i], sizeof(uint32_t) * RWm * d->sub);
-        if (e == cudaSuccess) e = cudaMalloc((void **)&d->succ[i], d->sub);
-        if (e == cudaSuccess) e = cudaMalloc((void **)&d->its[i], sizeof(int32_t) * d->sub);
-        if (e != cudaSuccess) {
-            set_error("decoder allocation: %s", cudaGetErrorString(e));
-            decoder_free(d);
-            return e == cudaErrorMemoryAllocation ? LDPC_ENOMEM : LDPC_ECUDA;
-        }
+    d->sub = sub_batch > 0 ? std::min(sub_batch, max_batch) : std::min(max_batch, 512);
+    // the largest sub-batch the plan can produce (the last chunk may absorb a remainder)
+    int32_t biggest = 0;
+    for (int32_t b : chunk_plan(max_batch, d->sub)) biggest = std::max(biggest, b);
+    d->ws_bytes = workspace_bytes(g, biggest);
+    const size_t RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32, MB = (size_t)max_batch;
+    cudaError_t e = cudaSuccess;
+    for (cudaStream_t *s : {&d->s_in, &d->s_comp, &d->s_out})
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&d->ws, d->ws_bytes);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->p, sizeof(double) * (size_t)g->n * MB);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->est, sizeof(uint32_t) * RWn * MB);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->syn, sizeof(uint32_t) * RWm * MB);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->succ, MB);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->its, sizeof(int32_t) * MB);
+    for (int i = 0; i < kMaxChunks && e == cudaSuccess; i++)
+        for (cudaEvent_t *ev : {&d->in_ready[i], &d->decoded[i]})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        set_error("decoder allocation: %s", cudaGetErrorString(e));
+        decoder_free(d);
+        return e == cudaErrorMemoryAllocation ? LDPC_ENOMEM : LDPC_ECUDA;
     }
     *out = d;
     return LDPC_OK;
@@ -415,42 +512,42 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
     const ldpc_graph *g = d->g;
     const size_t n = g->n, RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32;
+    const std::vector<int32_t> plan = chunk_plan(B, d->sub);
     int rc = LDPC_OK;
-    for (int32_t c0 = 0, i = 0; c0 < B && rc == LDPC_OK; c0 += d->sub, i++) {
-        const int slot = i & 1;
-        const int32_t b = std::min(d->sub, B - c0);
-        cudaStream_t s = d->st[slot];
-        cudaError_t e = cudaMemcpyAsync(d->p[slot], p_host + (size_t)c0 * n, sizeof(double) * n * b,
-                                        cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) {
-            set_error("H2D priors: %s", cudaGetErrorString(e));
-            rc = LDPC_ECUDA;
-            break;
+    cudaError_t e = cudaSuccess;
+    auto cuda = [&](cudaError_t x, const char *what) {
+        if (x != cudaSuccess && e == cudaSuccess) {
+            e = x;
+            set_error("%s: %s", what, cudaGetErrorString(x));
         }
-        rc = ldpc_decode(g, d->p[slot], b, max_iterations, flags, d->est[slot], d->succ[slot], d->its[slot],
-                         syn_bits_host ? d->syn[slot] : nullptr, d->ws[slot], d->ws_bytes, s, nullptr);
+    };
+    // 1. every H2D copy, back to back on the copy stream
+    for (size_t i = 0, c0 = 0; i < plan.size(); c0 += plan[i], i++) {
+        cuda(cudaMemcpyAsync(d->p + c0 * n, p_host + c0 * n, sizeof(double) * n * plan[i], cudaMemcpyHostToDevice,
+                             d->s_in), "H2D priors");
+        cuda(cudaEventRecord(d->in_ready[i], d->s_in), "record");
+    }
+    // 2. decodes in order, each results copy right behind its decode
+    for (size_t i = 0, c0 = 0; i < plan.size() && rc == LDPC_OK && e == cudaSuccess; c0 += plan[i], i++) {
+        const int32_t b = plan[i];
+        cuda(cudaStreamWaitEvent(d->s_comp, d->in_ready[i], 0), "wait input");
+        if (e != cudaSuccess) break;
+        rc = ldpc_decode(g, d->p + c0 * n, b, max_iterations, flags, d->est + c0 * RWn, d->succ + c0, d->its + c0,
+                         syn_bits_host ? d->syn + c0 * RWm : nullptr, d->ws, d->ws_bytes, d->s_comp, nullptr);
         if (rc) break;
-        e = cudaMemcpyAsync(est_bits_host + (size_t)c0 * RWn, d->est[slot], sizeof(uint32_t) * RWn * b,
-                            cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(success_host + c0, d->succ[slot], b, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(iters_host + c0, d->its[slot], sizeof(int32_t) * b, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess && syn_bits_host)
-            e = cudaMemcpyAsync(syn_bits_host + (size_t)c0 * RWm, d->syn[slot], sizeof(uint32_t) * RWm * b,
-                                cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) {
-            set_error("D2H results: %s", cudaGetErrorString(e));
-            rc = LDPC_ECUDA;
-        }
+        cuda(cudaEventRecord(d->decoded[i], d->s_comp), "record");
+        cuda(cudaStreamWaitEvent(d->s_out, d->decoded[i], 0), "wait decode");
+        cuda(cudaMemcpyAsync(est_bits_host + c0 * RWn, d->est + c0 * RWn, sizeof(uint32_t) * RWn * b,
+                             cudaMemcpyDeviceToHost, d->s_out), "D2H estimate");
+        cuda(cudaMemcpyAsync(success_host + c0, d->succ + c0, b, cudaMemcpyDeviceToHost, d->s_out), "D2H success");
+        cuda(cudaMemcpyAsync(iters_host + c0, d->its + c0, sizeof(int32_t) * b, cudaMemcpyDeviceToHost, d->s_out),
+             "D2H iterations");
+        if (syn_bits_host)
+            cuda(cudaMemcpyAsync(syn_bits_host + c0 * RWm, d->syn + c0 * RWm, sizeof(uint32_t) * RWm * b,
+                                 cudaMemcpyDeviceToHost, d->s_out), "D2H syndrome");
     }
-    for (int i = 0; i < 2; i++) {
-        cudaError_t e = cudaStreamSynchronize(d->st[i]);
-        if (e != cudaSuccess && rc == LDPC_OK) {
-            set_error("decode: %s", cudaGetErrorString(e));
-            rc = LDPC_ECUDA;
-        }
-    }
+    for (cudaStream_t s : {d->s_in, d->s_comp, d->s_out}) cuda(cudaStreamSynchronize(s), "decode");
+    if (rc == LDPC_OK && e != cudaSuccess) rc = LDPC_ECUDA;
     if (rc == LDPC_ECUDA) d->poisoned = true;  // mirrors engine.py:389-392: refuse further use
     return rc;
 }

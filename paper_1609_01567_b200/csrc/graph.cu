@@ -26,6 +26,7 @@ static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
     char buf[1024];
@@ -361,6 +362,8 @@ int build_ord(const int32_t *order, int32_t count, const int32_t *off, const int
 
 void free_graph(ldpc_graph *g) {
     if (!g) return;
+    for (auto &kv : g->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     cudaFree(g->var_slot_ord);
     cudaFree(g->chk_slot_ord);
     cudaFree(g->chk_var_ord);

@@ -10,14 +10,16 @@
 // Here every lane copies its 16-byte piece of each row with `cp.async.cg`
 // (LDGSTS: global -> shared, no register destination) into an S-stage ring
 // owned by the warp, so S-1 tasks per warp are in flight while the warp
-// computes the oldest one from shared memory.  Each lane reads back only the
-// bytes it copied itself, so the lane-local cp.async.wait_group is the only
-// synchronisation the data needs.  The row ids of a task are loaded one ring
-// step before its copies are issued, so index latency is off the critical path.
+// computes the oldest one from shared memory (cp.async.wait_group, then a
+// __syncwarp because with V=1 a lane reads pieces other lanes copied).  The
+// row ids of a task are loaded one ring step before its copies are issued, so
+// index latency is off the critical path.
 //
-// A task is (node, 64-codeword chunk); lane l owns codewords 2l, 2l+1 of the
-// chunk (16 bytes of each 512-byte row).  The grid is persistent: warp w of W
-// takes tasks w, w+W, ... in chunk-major order.
+// A task is (node, 32*V codewords), lane l owns codewords V*l .. V*l+V-1.  V=2
+// (16-byte rows pieces, 2 blocks/SM) suits low degrees; V=1 halves the
+// registers per lane so 3 blocks (24 warps) fit per SM, which the high-degree
+// variable buckets need to hide their fp64 dependency chains.  The grid is
+// persistent: warp w of W takes tasks w, w+W, ... in chunk-major order.
 #include <algorithm>
 #include <mutex>
 
@@ -26,19 +28,22 @@
 namespace ldpc {
 namespace {
 
-constexpr int kRow = 64;  // doubles per row (one slot x 64 codewords)
-
-// ring depth: ~13 KB of ring per warp (two 8-warp blocks per SM)
+// V = codewords per lane (1 or 2): a task is (node, 32*V codewords), a row is
+// 32*V doubles (256*V bytes).  Copies are always 16 bytes per lane, so a V=1
+// warp moves two rows per cp.async instruction.
+// ring depth from a per-warp budget (~13 KB at 16 warps/SM for V=2, ~9 KB at 24 warps/SM for V=1)
+template <int V>
 constexpr int ring_stages(int rows) {
-    const int s = (13 * 1024) / (rows * kRow * 8);
+    const int budget = V == 2 ? 13 * 1024 : 9 * 1024;
+    const int s = budget / (rows * 32 * V * 8);
     return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
-template <int ROWS>
+template <int ROWS, int V>
 struct Ring {
-    static constexpr int S = ring_stages(ROWS);
+    static constexpr int S = ring_stages<V>(ROWS);
     static constexpr size_t kIdsBytes = (size_t)S * 32 * sizeof(int);  // row ids per stage, one per lane
-    static constexpr size_t kBytes = kIdsBytes + (size_t)S * ROWS * kRow * sizeof(double);
+    static constexpr size_t kBytes = kIdsBytes + (size_t)S * ROWS * 32 * V * sizeof(double);
 };
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
@@ -51,14 +56,33 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__device__ __forceinline__ void st_cs2(double *p, double x, double y) {
-    __stcs(reinterpret_cast<double2 *>(p), make_double2(x, y));
+template <int V>
+__device__ __forceinline__ void st_v(double *p, const double (&o)[V]) {
+    if constexpr (V == 2) __stcs(reinterpret_cast<double2 *>(p), make_double2(o[0], o[1]));
+    else __stcs(p, o[0]);
 }
 
-__device__ __forceinline__ bool chunk64_done(const uint32_t *done, int ch) {
+template <int V>
+__device__ __forceinline__ void ld_smem(const double *p, double (&o)[V]) {
+    if constexpr (V == 2) {
+        const double2 x = *reinterpret_cast<const double2 *>(p);
+        o[0] = x.x;
+        o[1] = x.y;
+    } else {
+        o[0] = *p;
+    }
+}
+
+// all codewords of warp-chunk ch (32*V codewords) have stopped
+template <int V>
+__device__ __forceinline__ bool wchunk_done(const uint32_t *done, int ch) {
     if (done == nullptr) return false;
-    const uint2 d = *reinterpret_cast<const uint2 *>(done + 2 * ch);
-    return (d.x & d.y) == 0xffffffffu;
+    if constexpr (V == 2) {
+        const uint2 d = *reinterpret_cast<const uint2 *>(done + 2 * ch);
+        return (d.x & d.y) == 0xffffffffu;
+    } else {
+        return done[ch] == 0xffffffffu;
+    }
 }
 
 // Row ids of a task, one per lane:
@@ -75,73 +99,92 @@ __device__ __forceinline__ int load_id(const NodeLaunch &a, int64_t t, int lane)
     return 0;
 }
 
-template <int D, bool IS_VAR, bool FROM_PRIOR>
+template <int D, int V, bool IS_VAR, bool FROM_PRIOR>
 __device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *ids_s, int64_t t, int id, int lane) {
     constexpr int ROWS = D + (IS_VAR ? 1 : 0);
+    constexpr int ROW = 32 * V;                 // doubles per row
+    constexpr int RPI = V == 2 ? 1 : 2;         // rows per copy instruction
     const int ch = (int)(t / a.node_count);
     ids_s[lane] = id;
-    if (chunk64_done(a.done, ch)) return;  // nothing to fetch; compute skips it too
+    if (wchunk_done<V>(a.done, ch)) return;  // nothing to fetch; compute skips it too
+    const int cw0 = ch * 32 * V;
+    const int sub = V == 2 ? 0 : (lane >> 4);  // which row of the instruction's pair this lane copies
+    const int piece = V == 2 ? lane : (lane & 15);
 #pragma unroll
-    for (int r = 0; r < ROWS; r++) {
+    for (int j = 0; j < (ROWS + RPI - 1) / RPI; j++) {
+        const int r = j * RPI + sub;
+        // every lane takes part in the shuffles; lanes past the last row skip the copy
+        const int rr = r < ROWS ? r : ROWS - 1;
+        const int src_id = __shfl_sync(0xffffffffu, id, (IS_VAR && rr == D) ? D : ((!IS_VAR && FROM_PRIOR) ? 16 + rr : rr));
         const double *src;
-        if (IS_VAR && r == D) src = a.P + cofs(a.p_rows, __shfl_sync(0xffffffffu, id, D), ch * 64);
-        else if (!IS_VAR && FROM_PRIOR) src = a.P + cofs(a.p_rows, __shfl_sync(0xffffffffu, id, 16 + r), ch * 64);
-        else src = a.msg + cofs(a.msg_rows, __shfl_sync(0xffffffffu, id, r), ch * 64);
-        cp_async16(rows + r * kRow + 2 * lane, src + 2 * lane);
+        if ((IS_VAR && rr == D) || (!IS_VAR && FROM_PRIOR)) src = a.P + cofs(a.p_rows, src_id, cw0);
+        else src = a.msg + cofs(a.msg_rows, src_id, cw0);
+        if (r < ROWS) cp_async16(rows + r * ROW + 2 * piece, src + 2 * piece);
     }
 }
 
-template <int D>
+template <int D, int V>
 __device__ __forceinline__ void compute_check(const NodeLaunch &a, const double *rows, const int *ids, int ch,
                                               int lane) {
-    double b[D][2];
+    constexpr int ROW = 32 * V;
+    const int cw = ch * 32 * V + lane * V;
+    double b[D][V];
 #pragma unroll
     for (int i = 0; i < D; i++) {
-        const double2 q = *reinterpret_cast<const double2 *>(rows + i * kRow + 2 * lane);
-        b[i][0] = __dsub_rn(1.0, __dmul_rn(2.0, q.x));
-        b[i][1] = __dsub_rn(1.0, __dmul_rn(2.0, q.y));
+        double q[V];
+        ld_smem<V>(rows + i * ROW + V * lane, q);
+#pragma unroll
+        for (int v = 0; v < V; v++) b[i][v] = __dsub_rn(1.0, __dmul_rn(2.0, q[v]));
     }
-    double pre0 = 1.0, pre1 = 1.0;
+    double pre[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) pre[v] = 1.0;
 #pragma unroll
     for (int k = 0; k < D; k++) {
-        double acc0 = pre0, acc1 = pre1;
+        double out[V];
 #pragma unroll
-        for (int i = k + 1; i < D; i++) {
-            acc0 = __dmul_rn(acc0, b[i][0]);
-            acc1 = __dmul_rn(acc1, b[i][1]);
+        for (int v = 0; v < V; v++) {
+            double acc = pre[v];
+#pragma unroll
+            for (int i = k + 1; i < D; i++) acc = __dmul_rn(acc, b[i][v]);
+            out[v] = __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc)));
         }
-        st_cs2(a.msg + cofs(a.msg_rows, ids[k], ch * 64 + 2 * lane), __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc0))),
-               __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc1))));
+        st_v<V>(a.msg + cofs(a.msg_rows, ids[k], cw), out);
         if (k + 1 < D) {
-            pre0 = __dmul_rn(pre0, b[k][0]);
-            pre1 = __dmul_rn(pre1, b[k][1]);
+#pragma unroll
+            for (int v = 0; v < V; v++) pre[v] = __dmul_rn(pre[v], b[k][v]);
         }
     }
 }
 
-template <int D, bool WRITE_Q>
+template <int D, int V, bool WRITE_Q>
 __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *rows, const int *ids, int ch,
                                             int lane) {
-    double r[D][2], om[D][2];
+    constexpr int ROW = 32 * V;
+    const int cw = ch * 32 * V + lane * V;
+    double r[D][V], om[D][V];
 #pragma unroll
     for (int i = 0; i < D; i++) {
-        const double2 x = *reinterpret_cast<const double2 *>(rows + i * kRow + 2 * lane);
-        r[i][0] = x.x;
-        r[i][1] = x.y;
-        om[i][0] = __dsub_rn(1.0, x.x);
-        om[i][1] = __dsub_rn(1.0, x.y);
+        ld_smem<V>(rows + i * ROW + V * lane, r[i]);
+#pragma unroll
+        for (int v = 0; v < V; v++) om[i][v] = __dsub_rn(1.0, r[i][v]);
     }
-    const double2 pj = *reinterpret_cast<const double2 *>(rows + D * kRow + 2 * lane);
-    double p0[2] = {__dsub_rn(1.0, pj.x), __dsub_rn(1.0, pj.y)};
-    double p1[2] = {pj.x, pj.y};
+    double pj[V];
+    ld_smem<V>(rows + D * ROW + V * lane, pj);
+    double p0[V], p1[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        p0[v] = __dsub_rn(1.0, pj[v]);
+        p1[v] = pj[v];
+    }
     uint32_t slow = 0;
 #pragma unroll
     for (int k = 0; k < D; k++) {
         if constexpr (WRITE_Q) {
-            double out[2];
+            double out[V];
             bool all_ok = true;
 #pragma unroll
-            for (int v = 0; v < 2; v++) {
+            for (int v = 0; v < V; v++) {
                 double q0 = p0[v], q1 = p1[v];
 #pragma unroll
                 for (int i = k + 1; i < D; i++) {
@@ -152,25 +195,24 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
                 out[v] = ddiv_fast(q1, __dadd_rn(q0, q1), ok);  // den == 0 -> !ok
                 all_ok = all_ok && ok;
             }
-            if (all_ok) st_cs2(a.msg + cofs(a.msg_rows, ids[k], ch * 64 + 2 * lane), out[0], out[1]);
+            if (all_ok) st_v<V>(a.msg + cofs(a.msg_rows, ids[k], cw), out);
             else slow |= 1u << k;
         }
 #pragma unroll
-        for (int v = 0; v < 2; v++) {
+        for (int v = 0; v < V; v++) {
             p0[v] = __dmul_rn(p0[v], om[k][v]);
             p1[v] = __dmul_rn(p1[v], r[k][v]);
         }
     }
     if constexpr (WRITE_Q) {
         if (slow) {  // rare: tiny or zero denominators -> reference-order recompute, library division
-            const double pv[2] = {pj.x, pj.y};
 #pragma unroll
             for (int k = 0; k < D; k++) {
                 if (!((slow >> k) & 1u)) continue;
-                double out[2];
+                double out[V];
 #pragma unroll
-                for (int v = 0; v < 2; v++) {
-                    double q0 = __dsub_rn(1.0, pv[v]), q1 = pv[v];
+                for (int v = 0; v < V; v++) {
+                    double q0 = __dsub_rn(1.0, pj[v]), q1 = pj[v];
 #pragma unroll
                     for (int i = 0; i < D; i++) {
                         if (i == k) continue;
@@ -180,36 +222,49 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
                     const double den = __dadd_rn(q0, q1);
                     out[v] = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
                 }
-                st_cs2(a.msg + cofs(a.msg_rows, ids[k], ch * 64 + 2 * lane), out[0], out[1]);
+                st_v<V>(a.msg + cofs(a.msg_rows, ids[k], cw), out);
             }
         }
     }
-    // estimate (serial.py:132): bit = !(Q0 > Q1); two ballots -> natural codeword order
-    const uint32_t even = __ballot_sync(0xffffffffu, !(p0[0] > p1[0]));
-    const uint32_t odd = __ballot_sync(0xffffffffu, !(p0[1] > p1[1]));
-    if (lane == 0) {
-        uint32_t lo = part1by1(even) | (part1by1(odd) << 1);
-        uint32_t hi = part1by1(even >> 16) | (part1by1(odd >> 16) << 1);
-        uint32_t *dst = a.chat + (size_t)ids[D] * a.NW + 2 * ch;
-        if (a.done != nullptr) {
-            const uint32_t d0 = a.done[2 * ch], d1 = a.done[2 * ch + 1];
-            if (d0) lo = (lo & ~d0) | (dst[0] & d0);
-            if (d1) hi = (hi & ~d1) | (dst[1] & d1);
+    // estimate (serial.py:132): bit = !(Q0 > Q1)
+    uint32_t *row = a.chat + (size_t)ids[D] * a.NW;
+    if constexpr (V == 2) {
+        const uint32_t even = __ballot_sync(0xffffffffu, !(p0[0] > p1[0]));
+        const uint32_t odd = __ballot_sync(0xffffffffu, !(p0[1] > p1[1]));
+        if (lane == 0) {
+            uint32_t lo = part1by1(even) | (part1by1(odd) << 1);
+            uint32_t hi = part1by1(even >> 16) | (part1by1(odd >> 16) << 1);
+            uint32_t *dst = row + 2 * ch;
+            if (a.done != nullptr) {
+                const uint32_t d0 = a.done[2 * ch], d1 = a.done[2 * ch + 1];
+                if (d0) lo = (lo & ~d0) | (dst[0] & d0);
+                if (d1) hi = (hi & ~d1) | (dst[1] & d1);
+            }
+            *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
         }
-        *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
+    } else {
+        uint32_t bits = __ballot_sync(0xffffffffu, !(p0[0] > p1[0]));
+        if (lane == 0) {
+            if (a.done != nullptr) {
+                const uint32_t d0 = a.done[ch];
+                if (d0) bits = (bits & ~d0) | (row[ch] & d0);
+            }
+            row[ch] = bits;
+        }
     }
 }
 
-template <int D, bool IS_VAR, bool FLAG>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
-__global__ void __launch_bounds__(kThreads, 2) k_node_ring(NodeLaunch a, int64_t ntasks) {
+template <int D, int V, bool IS_VAR, bool FLAG>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
+__global__ void __launch_bounds__(kThreads, V == 2 ? 2 : 3) k_node_ring(NodeLaunch a, int64_t ntasks) {
     constexpr int ROWS = D + (IS_VAR ? 1 : 0);
+    constexpr int ROW = 32 * V;
     constexpr bool FP = !IS_VAR && FLAG;
-    using R = Ring<ROWS>;
+    using R = Ring<ROWS, V>;
     constexpr int S = R::S;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int *ids = reinterpret_cast<int *>(smem + (size_t)warp * R::kBytes);  // [S][32]
-    double *rows = reinterpret_cast<double *>(smem + (size_t)warp * R::kBytes + R::kIdsBytes);  // [S][ROWS][64]
+    double *rows = reinterpret_cast<double *>(smem + (size_t)warp * R::kBytes + R::kIdsBytes);  // [S][ROWS][ROW]
     const int64_t W = (int64_t)gridDim.x * kWarpsPerBlock;
     const int64_t first = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
 
@@ -219,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_node_ring(NodeLaunch a, int64_t
         const int64_t t = first + s * W;
         const int id = nid;
         if (t + W < ntasks) nid = load_id<D, IS_VAR, FP>(a, t + W, lane);
-        if (t < ntasks) issue<D, IS_VAR, FP>(a, rows + (size_t)s * ROWS * kRow, ids + s * 32, t, id, lane);
+        if (t < ntasks) issue<D, V, IS_VAR, FP>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, t, id, lane);
         cp_commit();
     }
     int it = 0;
@@ -229,26 +284,37 @@ __global__ void __launch_bounds__(kThreads, 2) k_node_ring(NodeLaunch a, int64_t
         const int sn = (it + S - 1) % S;
         const int id = nid;
         if (tn + W < ntasks) nid = load_id<D, IS_VAR, FP>(a, tn + W, lane);
-        if (tn < ntasks) issue<D, IS_VAR, FP>(a, rows + (size_t)sn * ROWS * kRow, ids + sn * 32, tn, id, lane);
+        if (tn < ntasks) issue<D, V, IS_VAR, FP>(a, rows + (size_t)sn * ROWS * ROW, ids + sn * 32, tn, id, lane);
         cp_commit();
         cp_wait<S - 1>();  // this lane's copies of task t have landed
-        __syncwarp();      // row ids of task t (written by their lanes) are visible
+        __syncwarp();      // ... and every other lane's (V=1 lanes read pieces copied by other lanes)
         const int s = it % S;
         const int ch = (int)(t / a.node_count);
-        if (!chunk64_done(a.done, ch)) {
-            if constexpr (IS_VAR) compute_var<D, FLAG>(a, rows + (size_t)s * ROWS * kRow, ids + s * 32, ch, lane);
-            else compute_check<D>(a, rows + (size_t)s * ROWS * kRow, ids + s * 32, ch, lane);
+        if (!wchunk_done<V>(a.done, ch)) {
+            if constexpr (IS_VAR) compute_var<D, V, FLAG>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, ch, lane);
+            else compute_check<D, V>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, ch, lane);
         }
         __syncwarp();  // stage s is reused by the issue of the next iteration
     }
     cp_wait<0>();
 }
 
-template <int D, bool IS_VAR, bool FLAG>
-int launch_ring(const NodeLaunch &a, cudaStream_t st) {
+int ring_v(bool var_side, int deg) {
+    static const int forced = [] {
+        const char *e = getenv("LDPC_RING_V");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced == 1 || forced == 2) return forced;
+    (void)var_side;
+    (void)deg;
+    return 2;  // V=1 measured slower for every bucket (profiles/r1_kernel_choice.md)
+}
+
+template <int D, int V, bool IS_VAR, bool FLAG>
+int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
     constexpr int ROWS = D + (IS_VAR ? 1 : 0);
-    const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS>::kBytes;
-    auto kern = k_node_ring<D, IS_VAR, FLAG>;
+    const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS, V>::kBytes;
+    auto kern = k_node_ring<D, V, IS_VAR, FLAG>;
     static int per_sm = -1, sms = 0;
     static std::mutex mu;
     {
@@ -267,13 +333,18 @@ int launch_ring(const NodeLaunch &a, cudaStream_t st) {
             per_sm = b;
         }
     }
-    const int64_t ntasks = (int64_t)a.node_count * (a.Bp / 64);
+    const int64_t ntasks = (int64_t)a.node_count * (a.Bp / (32 * V));
     if (ntasks == 0) return LDPC_OK;
     const int64_t need = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int64_t blocks = std::min<int64_t>(need, (int64_t)per_sm * sms);
     kern<<<(unsigned)blocks, kThreads, smem, st>>>(a, ntasks);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
+}
+
+template <int D, bool IS_VAR, bool FLAG>
+int launch_ring(const NodeLaunch &a, cudaStream_t st) {
+    return ring_v(IS_VAR, D) == 1 ? launch_ring_v<D, 1, IS_VAR, FLAG>(a, st) : launch_ring_v<D, 2, IS_VAR, FLAG>(a, st);
 }
 
 }  // namespace
