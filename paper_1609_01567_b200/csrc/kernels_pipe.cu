@@ -99,9 +99,18 @@ __device__ __forceinline__ int load_id(const NodeLaunch &a, int64_t t, int lane)
     return 0;
 }
 
+// Variables of degree >= kPriorRegDeg fetch their prior row into registers one
+// iteration ahead (their iterations are long enough to hide the latency, and the
+// smaller ring gains a stage); lower degrees stage the prior row in the ring.
+constexpr int kPriorRegDeg = 6;
+template <int D, bool IS_VAR>
+constexpr bool prior_in_ring() { return IS_VAR && D < kPriorRegDeg; }
+template <int D, bool IS_VAR>
+constexpr int ring_rows() { return D + (prior_in_ring<D, IS_VAR>() ? 1 : 0); }
+
 template <int D, int V, bool IS_VAR, bool FROM_PRIOR>
 __device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *ids_s, int64_t t, int id, int lane) {
-    constexpr int ROWS = D + (IS_VAR ? 1 : 0);
+    constexpr int ROWS = ring_rows<D, IS_VAR>();
     constexpr int ROW = 32 * V;                 // doubles per row
     constexpr int RPI = V == 2 ? 1 : 2;         // rows per copy instruction
     const int ch = (int)(t / a.node_count);
@@ -115,10 +124,9 @@ __device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *id
         const int r = j * RPI + sub;
         // every lane takes part in the shuffles; lanes past the last row skip the copy
         const int rr = r < ROWS ? r : ROWS - 1;
-        const int src_id = __shfl_sync(0xffffffffu, id, (IS_VAR && rr == D) ? D : ((!IS_VAR && FROM_PRIOR) ? 16 + rr : rr));
-        const double *src;
-        if ((IS_VAR && rr == D) || (!IS_VAR && FROM_PRIOR)) src = a.P + cofs(a.p_rows, src_id, cw0);
-        else src = a.msg + cofs(a.msg_rows, src_id, cw0);
+        const bool prior_row = (prior_in_ring<D, IS_VAR>() && rr == D) || (!IS_VAR && FROM_PRIOR);
+        const int src_id = __shfl_sync(0xffffffffu, id, (!IS_VAR && FROM_PRIOR) ? 16 + rr : rr);
+        const double *src = prior_row ? a.P + cofs(a.p_rows, src_id, cw0) : a.msg + cofs(a.msg_rows, src_id, cw0);
         if (r < ROWS) cp_async16(rows + r * ROW + 2 * piece, src + 2 * piece);
     }
 }
@@ -159,7 +167,7 @@ __device__ __forceinline__ void compute_check(const NodeLaunch &a, const double 
 
 template <int D, int V, bool WRITE_Q>
 __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *rows, const int *ids, int ch,
-                                            int lane) {
+                                            int lane, const double (&pj)[V]) {
     constexpr int ROW = 32 * V;
     const int cw = ch * 32 * V + lane * V;
     double r[D][V], om[D][V];
@@ -169,8 +177,6 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
 #pragma unroll
         for (int v = 0; v < V; v++) om[i][v] = __dsub_rn(1.0, r[i][v]);
     }
-    double pj[V];
-    ld_smem<V>(rows + D * ROW + V * lane, pj);
     double p0[V], p1[V];
 #pragma unroll
     for (int v = 0; v < V; v++) {
@@ -254,9 +260,23 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
     }
 }
 
+// a variable's prior row (V doubles per lane) straight into registers
+template <int V>
+__device__ __forceinline__ void load_prior(const NodeLaunch &a, int node, int ch, int lane, double (&o)[V]) {
+    const double *p = a.P + cofs(a.p_rows, node, ch * 32 * V + V * lane);
+    if constexpr (V == 2) {
+        const double2 x = __ldg(reinterpret_cast<const double2 *>(p));
+        o[0] = x.x;
+        o[1] = x.y;
+    } else {
+        o[0] = __ldg(p);
+    }
+}
+
 template <int D, int V, bool IS_VAR, bool FLAG>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
 __global__ void __launch_bounds__(kThreads, V == 2 ? 2 : 3) k_node_ring(NodeLaunch a, int64_t ntasks) {
-    constexpr int ROWS = D + (IS_VAR ? 1 : 0);
+    constexpr int ROWS = ring_rows<D, IS_VAR>();
+    constexpr bool PREG = IS_VAR && !prior_in_ring<D, IS_VAR>();  // prior via registers
     constexpr int ROW = 32 * V;
     constexpr bool FP = !IS_VAR && FLAG;
     using R = Ring<ROWS, V>;
@@ -277,6 +297,13 @@ __global__ void __launch_bounds__(kThreads, V == 2 ? 2 : 3) k_node_ring(NodeLaun
         if (t < ntasks) issue<D, V, IS_VAR, FP>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, t, id, lane);
         cp_commit();
     }
+    // variables: the prior row of the task being computed is loaded into registers
+    // one iteration ahead (it was issued S-1 >= 1 iterations ago, so its id is in smem)
+    double pnext[V] = {};
+    if (PREG && first < ntasks) {
+        __syncwarp();  // row ids written at issue (plain shared stores) are visible
+        load_prior<V>(a, ids[D], (int)(first / a.node_count), lane, pnext);
+    }
     int it = 0;
     for (int64_t t = first; t < ntasks; t += W, it++) {
         // keep S-1 tasks in flight: issue task t + (S-1) W into the stage freed last iteration
@@ -290,8 +317,19 @@ __global__ void __launch_bounds__(kThreads, V == 2 ? 2 : 3) k_node_ring(NodeLaun
         __syncwarp();      // ... and every other lane's (V=1 lanes read pieces copied by other lanes)
         const int s = it % S;
         const int ch = (int)(t / a.node_count);
+        double pj[V];
+        if constexpr (PREG) {
+#pragma unroll
+            for (int v = 0; v < V; v++) pj[v] = pnext[v];
+        } else if constexpr (IS_VAR) {
+            ld_smem<V>(rows + (size_t)s * ROWS * ROW + D * ROW + V * lane, pj);
+        }
+        if (PREG && t + W < ntasks) {
+            const int s1 = (it + 1) % S;  // task t + W was issued at least one iteration ago
+            load_prior<V>(a, ids[s1 * 32 + D], (int)((t + W) / a.node_count), lane, pnext);
+        }
         if (!wchunk_done<V>(a.done, ch)) {
-            if constexpr (IS_VAR) compute_var<D, V, FLAG>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, ch, lane);
+            if constexpr (IS_VAR) compute_var<D, V, FLAG>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, ch, lane, pj);
             else compute_check<D, V>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, ch, lane);
         }
         __syncwarp();  // stage s is reused by the issue of the next iteration
@@ -312,7 +350,7 @@ int ring_v(bool var_side, int deg) {
 
 template <int D, int V, bool IS_VAR, bool FLAG>
 int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
-    constexpr int ROWS = D + (IS_VAR ? 1 : 0);
+    constexpr int ROWS = ring_rows<D, IS_VAR>();
     const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS, V>::kBytes;
     auto kern = k_node_ring<D, V, IS_VAR, FLAG>;
     static int per_sm = -1, sms = 0;

@@ -63,7 +63,7 @@ __device__ __forceinline__ void put_bits(uint32_t *dst, uint32_t bits, const uin
 }
 
 template <int D, int V, bool WRITE_Q>
-__global__ void __launch_bounds__(kThreads) k_var_reg(NodeLaunch a) {
+__global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_reg(NodeLaunch a) {
     const int lane = threadIdx.x & 31;
     const int chunks = a.Bp / (32 * V);
     const int64_t task = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);

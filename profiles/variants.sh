@@ -1,6 +1,6 @@
 #!/bin/bash
 # Quick A/B of kernel policies on the bench workload (device-timed value + per-class kernel ms).
-for cfg in "LDPC_KERNEL=reg" ${EXTRA_VARIANTS:-}; do
+for cfg in "DEFAULT=1" ${EXTRA_VARIANTS:-}; do
   cfg=${cfg//,/ }
   env $cfg timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/v.json 2>gpurun_out/v.err
   python -c "
