@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--ebno", type=float, default=2.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-fast", action="store_true", help="skip the fp32 fast-mode leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--sub-batch", type=int, default=0, help="e2e pipeline sub-batch (0 = decoder default)")
     return ap.parse_args()
@@ -323,6 +324,25 @@ def run_ours(args):
                "path": "ParallelDecoder.decode_priors (ldpc_decoder_decode_host: pinned H2D, decode, D2H, "
                        "pipelined over 2 streams)"}
 
+    # f4 fast mode (fp32, not bit-exact): same workload, device-timed, agreement with the exact run
+    fast = None
+    if not args.no_fast and H.total_edges and max(H.degrees()[0].max(), H.degrees()[1].max()) <= 16:
+        outs32 = dec.alloc_outputs(B, dev)
+        for _ in range(args.warmup):
+            dec.decode_device(P_dev, iters, early_stop=False, workspace=ws, outputs=outs32, precision="fp32")
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            dec.decode_device(P_dev, iters, early_stop=False, workspace=ws, outputs=outs32, precision="fp32")
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1) / args.steps
+        same = (outs32[0] == outs[0]).all(dim=1).float().mean().item()
+        fast = {"value": world * B * H.n / (fms / 1e3) / 1e9, "unit": UNIT, "dtype": "f32", "ms_per_step": fms,
+                "identical_frames_vs_f64": same,
+                "note": "f4 fast mode: same algorithm in fp32 (not bit-exact; tolerance in DESIGN.md)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, frames, secs = cpu_reference_rate(H, P_host, iters, args.cpu_seconds)
@@ -347,6 +367,7 @@ def run_ours(args):
                          "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in pd.items()}},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "fast_fp32": fast,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "counts": {"bit_errors": int(counts[0]), "failures": int(counts[1]), "iterations": int(counts[2]),

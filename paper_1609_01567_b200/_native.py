@@ -22,6 +22,7 @@ LDPC_ECLOSED = -4
 
 FLAG_EARLY_STOP = 0
 FLAG_FIXED_ITERS = 1
+FLAG_FP32 = 2
 
 VARIABLE = 0
 CHECK = 1
@@ -73,6 +74,8 @@ def _declare(L):
     L.ldpc_decoder_decode_host.argtypes = [vp, vp, i32, i32, u32, vp, vp, vp, vp]
     L.ldpc_decoder_destroy.argtypes = [vp]
     L.ldpc_decoder_destroy.restype = None
+    L.ldpc_phase_f32.argtypes = [vp, ctypes.c_int, vp, vp, vp, i32, vp, sz, vp]
+    L.ldpc_phase_f32.restype = ctypes.c_int
     L.ldpc_selftest_division.argtypes = [ctypes.c_uint64, i64, P_i64]
     L.ldpc_selftest_division.restype = ctypes.c_int
     for name in ("ldpc_graph_create", "ldpc_graph_info", "ldpc_graph_get_tables", "ldpc_graph_get_var_groups",

@@ -157,8 +157,23 @@ NodeLaunch var_args(const ldpc_graph *g, const Workspace &w, const uint32_t *don
                       (int32_t)g->E, g->n, g->var_slot, g->var_slot_ord, nullptr, 0};
 }
 
-int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const uint32_t *done, cudaStream_t s) {
+// fp32 fast mode (LDPC_FLAG_FP32): fp32 messages and priors live in the fp64 message buffer
+float *msg32(const ldpc_graph *g, const Workspace &w) { return reinterpret_cast<float *>(w.msg); }
+float *prior32(const ldpc_graph *g, const Workspace &w) { return reinterpret_cast<float *>(w.msg) + (size_t)g->E * w.Bp; }
+
+int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const uint32_t *done, cudaStream_t s,
+                bool fast = false) {
     NodeLaunch a = check_args(g, w, done);
+    if (fast) {
+        for (const Bucket &b : g->chk_buckets) {
+            a.node_begin = b.node_begin;
+            a.node_count = b.node_count;
+            a.edge_begin = b.edge_begin;
+            int rc = launch_check_f32(a, b.deg, from_prior, msg32(g, w), prior32(g, w), s);
+            if (rc) return rc;
+        }
+        return LDPC_OK;
+    }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
     for (const Bucket &b : g->chk_buckets) {
         if (b.deg <= kMaxRegDegree) {
@@ -182,8 +197,19 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
     return LDPC_OK;
 }
 
-int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint32_t *done, cudaStream_t s) {
+int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint32_t *done, cudaStream_t s,
+              bool fast = false) {
     NodeLaunch a = var_args(g, w, done);
+    if (fast) {
+        for (const Bucket &b : g->var_buckets) {
+            a.node_begin = b.node_begin;
+            a.node_count = b.node_count;
+            a.edge_begin = b.edge_begin;
+            int rc = launch_var_f32(a, b.deg, write_q, msg32(g, w), prior32(g, w), s);
+            if (rc) return rc;
+        }
+        return LDPC_OK;
+    }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
     for (const Bucket &b : g->var_buckets) {
         if (b.deg <= kMaxRegDegree) {
@@ -228,25 +254,31 @@ int init_flags(const Workspace &w, bool early, cudaStream_t s) {
 }  // namespace
 
 // The decode proper on a carved workspace whose P is filled.
-int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s, Prof &prof) {
+int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s, Prof &prof,
+               bool fast = false) {
     const int64_t B = w.B, E = g->E, n = g->n, m = g->m;
-    const int64_t c_bytes = 16 * E * B;                   // read q (or p-gather) + write r
-    const int64_t ve_bytes = (16 * E + 8 * n + n / 8) * B; // read r, p; write q, c_hat bits
-    const int64_t e_bytes = (8 * E + 8 * n + n / 8) * B;   // read r, p; write c_hat bits
-    const int64_t s_bytes = (n / 8) * B;                  // read c_hat bits
+    const int64_t wb = fast ? 4 : 8;                         // message / prior width in bytes
+    const int64_t c_bytes = 2 * wb * E * B;                  // read q (or p-gather) + write r
+    const int64_t ve_bytes = (2 * wb * E + wb * n + n / 8) * B; // read r, p; write q, c_hat bits
+    const int64_t e_bytes = (wb * E + wb * n + n / 8) * B;   // read r, p; write c_hat bits
+    const int64_t s_bytes = (n / 8) * B;                     // read c_hat bits
     int rc = init_flags(w, early, s);
     if (rc) return rc;
+    if (fast) {
+        rc = launch_priors_to_f32(w.P, prior32(g, w), (size_t)g->n * w.Bp, s);
+        if (rc) return rc;
+    }
     const uint32_t *done = early ? w.done : nullptr;
-    RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, true, nullptr, s));
+    RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, true, nullptr, s, fast));
     for (int32_t t = 1; t <= max_iter; t++) {
-        RUN(LDPC_KCLASS_VARIABLE, ve_bytes, var_phase(g, w, true, done, s));
+        RUN(LDPC_KCLASS_VARIABLE, ve_bytes, var_phase(g, w, true, done, s, fast));
         if (early) {
             RUN(LDPC_KCLASS_SYNDROME, s_bytes, launch_syndrome(g, w, false, true, s));
             RUN(LDPC_KCLASS_SYNDROME, 0, launch_update_done(w, t - 1, false, s));
         }
-        RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, false, done, s));
+        RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, false, done, s, fast));
     }
-    RUN(LDPC_KCLASS_ESTIMATE, e_bytes, var_phase(g, w, false, done, s));
+    RUN(LDPC_KCLASS_ESTIMATE, e_bytes, var_phase(g, w, false, done, s, fast));
     RUN(LDPC_KCLASS_SYNDROME, s_bytes + (m / 8) * B, launch_syndrome(g, w, true, early, s));
     if (early) RUN(LDPC_KCLASS_SYNDROME, 0, launch_update_done(w, max_iter, true, s));
     (void)m;
@@ -269,7 +301,10 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
     LDPC_ARG_CHECK(g != nullptr, "NULL graph");
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
     LDPC_ARG_CHECK(p_dev && est_bits_dev && success_dev && iters_dev, "NULL output/input pointer");
-    LDPC_ARG_CHECK(flags <= LDPC_FLAG_FIXED_ITERS, "unknown flags 0x%x", flags);
+    LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32)) == 0, "unknown flags 0x%x", flags);
+    const bool fast = (flags & LDPC_FLAG_FP32) != 0;
+    LDPC_ARG_CHECK(!fast || (g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree),
+                   "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
     Workspace w;
     int rc = carve_workspace(g, B, workspace_dev, workspace_bytes_, &w);
     if (rc) return rc;
@@ -278,7 +313,7 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
     auto sequence = [&](Prof &prof) -> int {
         const int64_t n = g->n, m = g->m;
         RUN(LDPC_KCLASS_LAYOUT, 16 * n * B, launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s));
-        int r = run_decode(g, w, max_iterations, early, s, prof);
+        int r = run_decode(g, w, max_iterations, early, s, prof, fast);
         if (r) return r;
         RUN(LDPC_KCLASS_LAYOUT, (n / 8) * 2 * B, launch_pack_rows(w.chat, g->n, w.NW, B, est_bits_dev, s));
         if (syn_bits_dev)
@@ -398,6 +433,27 @@ extern "C" int ldpc_phase_syndrome(const ldpc_graph *g, const uint8_t *chat_dev,
     LDPC_CUDA_TRY(cudaMemsetAsync(w.unsat, 0, sizeof(uint32_t) * w.NW, s));
     if ((rc = launch_syndrome(g, w, true, false, s))) return rc;
     return launch_bits_to_bytes(w.zb, g->m, w.NW, B, z_dev, s);
+}
+
+// fp32 fast-mode single phases (message tolerance tests): inputs/outputs fp64 canonical order
+extern "C" int ldpc_phase_f32(const ldpc_graph *g, int phase, const double *p_dev, const double *in_dev,
+                              double *out_dev, int32_t B, void *ws, size_t ws_bytes, void *stream) {
+    LDPC_ARG_CHECK(g && in_dev && out_dev && (phase == 1 || p_dev), "NULL argument");
+    LDPC_ARG_CHECK(phase == 0 || phase == 1, "phase must be 0 (to check) or 1 (to variable)");
+    LDPC_ARG_CHECK(g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree,
+                   "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
+    Workspace w;
+    int rc = carve_workspace(g, B, ws, ws_bytes, &w);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (phase == 0) {
+        if ((rc = launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s))) return rc;
+        if ((rc = launch_priors_to_f32(w.P, prior32(g, w), (size_t)g->n * w.Bp, s))) return rc;
+    }
+    if ((rc = launch_canon_to_slots_f32(g, in_dev, B, msg32(g, w), w.Bp, s))) return rc;
+    rc = phase == 0 ? var_phase(g, w, true, nullptr, s, true) : check_phase(g, w, false, nullptr, s, true);
+    if (rc) return rc;
+    return launch_slots_to_canon_f32(g, msg32(g, w), w.Bp, out_dev, B, s);
 }
 
 // ---- host-buffer decoder: pipelined H2D / decode / D2H ------------------------

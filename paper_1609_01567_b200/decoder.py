@@ -157,37 +157,58 @@ def _dev(a: np.ndarray, device: int):
 
 # ---- single phases (serial.py:63-147 signatures, any batch) -------------------
 
-def values_to_check(p, r, tables: CodeTables) -> np.ndarray:
-    """V-phase (serial.py:63-89) on the GPU; p [n] or [B,n], r [E] or [B,E] canonical order."""
+def _flags(early_stop: bool, precision: str) -> int:
+    if precision not in ("fp64", "fp32"):
+        raise ValueError("precision must be 'fp64' (exact) or 'fp32' (fast mode)")
+    return ((_native.FLAG_EARLY_STOP if early_stop else _native.FLAG_FIXED_ITERS)
+            | (_native.FLAG_FP32 if precision == "fp32" else 0))
+
+
+def values_to_check(p, r, tables: CodeTables, precision: str = "fp64") -> np.ndarray:
+    """V-phase (serial.py:63-89) on the GPU; p [n] or [B,n], r [E] or [B,E] canonical order.
+
+    precision="fp32" runs the fast-mode kernel (not bit-exact; DESIGN.md states the tolerance)."""
     T = _tables_of(tables)
     P, single = _as_batch(p, T.n, "priors")
     R, _ = _as_batch(r, T.total_edges, "messages")
     if P.shape[0] != R.shape[0]:
         raise ValueError("batch mismatch between p and r")
+    _flags(True, precision)
     B = P.shape[0]
     g = T.graph
     torch = _torch()
     ws, nb = _workspace(g, B)
     dp, dr = _dev(P, g.device), _dev(R, g.device)
     dq = torch.empty_like(dr)
-    _native.check(_native.lib().ldpc_phase_to_check(g.handle, _ptr(dp), _ptr(dr), _ptr(dq), B, _ptr(ws), nb,
-                                                    _native.current_stream_handle()), "values_to_check")
+    if precision == "fp32":
+        rc = _native.lib().ldpc_phase_f32(g.handle, 0, _ptr(dp), _ptr(dr), _ptr(dq), B, _ptr(ws), nb,
+                                          _native.current_stream_handle())
+    else:
+        rc = _native.lib().ldpc_phase_to_check(g.handle, _ptr(dp), _ptr(dr), _ptr(dq), B, _ptr(ws), nb,
+                                               _native.current_stream_handle())
+    _native.check(rc, "values_to_check")
     q = dq.cpu().numpy()
     return q[0] if single else q
 
 
-def values_to_variable(q, tables: CodeTables) -> np.ndarray:
-    """C-phase (serial.py:92-112) on the GPU; q [E] or [B,E] canonical order."""
+def values_to_variable(q, tables: CodeTables, precision: str = "fp64") -> np.ndarray:
+    """C-phase (serial.py:92-112) on the GPU; q [E] or [B,E] canonical order (precision as values_to_check)."""
     T = _tables_of(tables)
     Q, single = _as_batch(q, T.total_edges, "messages")
+    _flags(True, precision)
     B = Q.shape[0]
     g = T.graph
     torch = _torch()
     ws, nb = _workspace(g, B)
     dq = _dev(Q, g.device)
     dr = torch.empty_like(dq)
-    _native.check(_native.lib().ldpc_phase_to_variable(g.handle, _ptr(dq), _ptr(dr), B, _ptr(ws), nb,
-                                                       _native.current_stream_handle()), "values_to_variable")
+    if precision == "fp32":
+        rc = _native.lib().ldpc_phase_f32(g.handle, 1, None, _ptr(dq), _ptr(dr), B, _ptr(ws), nb,
+                                          _native.current_stream_handle())
+    else:
+        rc = _native.lib().ldpc_phase_to_variable(g.handle, _ptr(dq), _ptr(dr), B, _ptr(ws), nb,
+                                                  _native.current_stream_handle())
+    _native.check(rc, "values_to_variable")
     r = dr.cpu().numpy()
     return r[0] if single else r
 
@@ -305,18 +326,20 @@ class ParallelDecoder:
         return self.decode_priors(p.reshape(1, -1), max_iterations)[0]
 
     def decode_batch(self, Y, sigma2, max_iterations: int = DEFAULT_MAX_ITERATIONS,
-                     early_stop: bool = True) -> BatchResult:
+                     early_stop: bool = True, precision: str = "fp64") -> BatchResult:
         """B received frames [B, n] (sigma2 scalar or [B]) -> BatchResult."""
         if self._closed:
             raise RuntimeError("decoder is closed")
         Y = np.asarray(Y, dtype=np.float64)
         if Y.ndim != 2 or Y.shape[1] != self.tables.n:
             raise ValueError(f"expected frames of {self.tables.n} observations")
-        return self.decode_priors(priors_awgn_batch(Y, sigma2), max_iterations, early_stop)
+        return self.decode_priors(priors_awgn_batch(Y, sigma2), max_iterations, early_stop, precision=precision)
 
     def decode_priors(self, P, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
-                      out: BatchResult | None = None) -> BatchResult:
-        """Host priors [B, n] (pinned memory recommended) -> host BatchResult."""
+                      out: BatchResult | None = None, precision: str = "fp64") -> BatchResult:
+        """Host priors [B, n] (pinned memory recommended) -> host BatchResult.
+
+        precision="fp32": fast mode, same algorithm in fp32 (not bit-exact; DESIGN.md tolerance)."""
         if self._closed:
             raise RuntimeError("decoder is closed")
         if max_iterations < 0:
@@ -330,7 +353,7 @@ class ParallelDecoder:
                                                       np.empty(B, np.uint8), np.empty(B, np.int32),
                                                       np.empty((B, (m + 31) // 32), np.uint32), n, m)
         L = _native.lib()
-        flags = _native.FLAG_EARLY_STOP if early_stop else _native.FLAG_FIXED_ITERS
+        flags = _flags(early_stop, precision)
         with self._lock:
             for c0 in range(0, B, self.max_batch):
                 c1 = min(B, c0 + self.max_batch)
@@ -344,7 +367,8 @@ class ParallelDecoder:
         return res
 
     def decode_device(self, P_dev, max_iterations: int, early_stop: bool = True, workspace=None,
-                      outputs=None, profile: "_native.Profile | None" = None, syndrome_out: bool = True):
+                      outputs=None, profile: "_native.Profile | None" = None, syndrome_out: bool = True,
+                      precision: str = "fp64"):
         """Device priors tensor [B, n] fp64 -> device tensors (est_bits, success, iters, syn_bits).
 
         Stream-ordered on torch's current stream; no host synchronisation
@@ -364,7 +388,7 @@ class ParallelDecoder:
         if outputs is None:
             outputs = self.alloc_outputs(B, P_dev.device)
         est, ok, its, syn = outputs
-        flags = _native.FLAG_EARLY_STOP if early_stop else _native.FLAG_FIXED_ITERS
+        flags = _flags(early_stop, precision)
         rc = _native.lib().ldpc_decode(g.handle, _ptr(P_dev), B, int(max_iterations), flags, _ptr(est), _ptr(ok),
                                        _ptr(its), _ptr(syn) if syndrome_out else None, _ptr(workspace), nb,
                                        _native.current_stream_handle(),

@@ -1,3 +1,5 @@
-timeout 600 python -m pytest tests -q -m gpu --timeout 600 -p no:cacheprovider -x 2>&1 | tail -1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(check|var|node)" -c 40 --csv --log-file gpurun_out/launches_x.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > /dev/null 2>&1
-bash profiles/variants.sh
+python tools/fp32_tolerance.py > gpurun_out/fp32_tol.json 2>&1; cat gpurun_out/fp32_tol.json | tail -80
+for prec in fp32; do
+timeout 600 python -c "
+import sys; sys.argv=['bench.py','--steps','10','--warmup','3','--no-cpu','--no-e2e']
+" ; done
