@@ -199,13 +199,20 @@ def gpu_decode_counts(decoder):
 
 def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int = 0,
               batch: int = DEFAULT_BATCH, rate: float | None = None, decode_fn=None,
-              exact_channel: bool = False, device=None) -> list[BerPoint]:
+              exact_channel: bool = False, device=None, channel: str = "host",
+              precision: str = "fp64") -> list[BerPoint]:
     """channel.py:83-137 on the GPU, frames sharded over torch.distributed ranks.
 
     decode_fn(Y [b, n], sigma2, max_iterations, counts) must add
     [bit errors, failures, iterations, frames] of the batch into the int64[4]
     tensor ``counts``; the default decodes on this rank's GPU.
+    channel="device" (f1) generates the noise and priors on the GPU as well
+    (integer-exact RNG streams, device transcendentals: statistical parity).
     """
+    if channel not in ("host", "device"):
+        raise ValueError("channel must be 'host' or 'device'")
+    if channel == "device":
+        return _ber_sweep_device(H, ebno_points, frames, max_iterations, seed, batch, rate, precision)
     import torch
 
     if frames < 1:
@@ -243,6 +250,40 @@ def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int =
     finally:
         if decoder is not None:
             decoder.close()
+    return points
+
+
+def _ber_sweep_device(H, ebno_points, frames, max_iterations, seed, batch, rate, precision):
+    """f1 path: channel, priors, decode and the error fold all on this rank's GPU."""
+    import torch
+
+    from .decoder import ParallelDecoder
+    from .tables import CodeTables
+
+    if frames < 1:
+        raise ValueError("frames must be at least 1")
+    dist, rank, world = _dist_info()
+    R = rate if rate is not None else (H.n - H.m) / H.n
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lo, hi = shard_range(frames, rank, world)
+    points = []
+    with ParallelDecoder(CodeTables.from_matrix(H), max_batch=batch) as dec:
+        ws = dec.workspace(batch)
+        outs = dec.alloc_outputs(batch, dev)
+        for index, ebno_db in enumerate(ebno_points):
+            sigma2 = ebno_to_sigma2(float(ebno_db), R)
+            counts = torch.zeros(4, dtype=torch.int64, device=dev)
+            for b0 in range(lo, hi, batch):
+                b = min(hi, b0 + batch) - b0
+                o = tuple(x[:b] for x in outs)
+                dec.decode_channel(seed, index, b0, b, sigma2, max_iterations, workspace=ws, outputs=o,
+                                   precision=precision)
+                dec.count_errors(o, counts)
+            if dist is not None:
+                dist.all_reduce(counts)
+            c = [int(x) for x in counts.cpu().tolist()]
+            points.append(BerPoint(ebno_db=float(ebno_db), sigma2=sigma2, frames=frames, bit_errors=c[0],
+                                   ber=c[0] / (frames * H.n), mean_iterations=c[2] / frames, failures=c[1]))
     return points
 
 

@@ -375,6 +375,32 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
     return prof.flush();
 }
 
+// f1: channel prologue on the device (noise + priors), then the same decode sequence
+extern "C" int ldpc_decode_channel(const ldpc_graph *g, uint64_t seed, uint64_t point, uint64_t frame0, int32_t B,
+                                   double sigma2, int32_t max_iterations, uint32_t flags, uint32_t *est_bits_dev,
+                                   uint8_t *success_dev, int32_t *iters_dev, uint32_t *syn_bits_dev,
+                                   void *workspace_dev, size_t workspace_bytes_, void *stream) {
+    LDPC_ARG_CHECK(g != nullptr, "NULL graph");
+    LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
+    LDPC_ARG_CHECK(sigma2 > 0.0, "sigma2 must be positive");
+    LDPC_ARG_CHECK(est_bits_dev && success_dev && iters_dev, "NULL output pointer");
+    LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32)) == 0, "unknown flags 0x%x", flags);
+    const bool fast = (flags & LDPC_FLAG_FP32) != 0;
+    LDPC_ARG_CHECK(!fast || (g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree),
+                   "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
+    Workspace w;
+    int rc = carve_workspace(g, B, workspace_dev, workspace_bytes_, &w);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
+    Prof prof;
+    if ((rc = launch_channel_priors(seed, point, frame0, B, g->n, sigma2, w.P, w.Bp, s))) return rc;
+    if ((rc = run_decode(g, w, max_iterations, early, s, prof, fast))) return rc;
+    if ((rc = launch_pack_rows(w.chat, g->n, w.NW, B, est_bits_dev, s))) return rc;
+    if (syn_bits_dev && (rc = launch_pack_rows(w.zb, g->m, w.NW, B, syn_bits_dev, s))) return rc;
+    return launch_finalize(w, early, max_iterations, success_dev, iters_dev, s);
+}
+
 extern "C" int ldpc_count_errors(const ldpc_graph *g, const uint32_t *est_bits_dev, const uint8_t *success_dev,
                                  const int32_t *iters_dev, int32_t B, int64_t *counts_dev, void *stream) {
     LDPC_ARG_CHECK(g && est_bits_dev && success_dev && iters_dev && counts_dev, "NULL argument");

@@ -396,6 +396,30 @@ class ParallelDecoder:
         _native.check(rc, "ldpc_decode")
         return outputs
 
+    def decode_channel(self, seed: int, point: int, frame0: int, B: int, sigma2: float, max_iterations: int,
+                       early_stop: bool = True, workspace=None, outputs=None, precision: str = "fp64"):
+        """f1: frames frame0..frame0+B-1 of Eb/N0 point `point` generated on the device (all-zero
+        codeword over AWGN, the reference's per-frame xorshift128+ streams) and decoded; device outputs."""
+        if self._closed:
+            raise RuntimeError("decoder is closed")
+        if sigma2 <= 0:
+            raise ValueError("sigma2 must be positive")
+        g = self.tables.graph
+        torch = _torch()
+        if workspace is None:
+            workspace, nb = _workspace(g, B)
+        else:
+            nb = workspace.numel()
+        if outputs is None:
+            outputs = self.alloc_outputs(B, torch.device("cuda", g.device))
+        est, ok, its, syn = outputs
+        rc = _native.lib().ldpc_decode_channel(g.handle, int(seed) & (2**64 - 1), int(point), int(frame0), int(B),
+                                               float(sigma2), int(max_iterations), _flags(early_stop, precision),
+                                               _ptr(est), _ptr(ok), _ptr(its), None, _ptr(workspace), nb,
+                                               _native.current_stream_handle())
+        _native.check(rc, "ldpc_decode_channel")
+        return outputs
+
     def alloc_outputs(self, B: int, device):
         torch = _torch()
         n, m = self.tables.n, self.tables.m
