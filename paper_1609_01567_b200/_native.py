@@ -8,11 +8,13 @@ with ``python -m paper_1609_01567_b200.build`` (or __graft_entry__.build()).
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 import threading
 
 _HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_native" / "libldpc_b200.so"
+# LDPC_LIB selects an alternative build of the same library (A/B layout experiments)
+LIB_PATH = pathlib.Path(os.environ["LDPC_LIB"]) if os.environ.get("LDPC_LIB") else _HERE / "_native" / "libldpc_b200.so"
 
 LDPC_OK = 0
 LDPC_EINVAL = -1

@@ -36,8 +36,8 @@ bool graphs_enabled() {
 
 // Kernel family per (side, degree) for the register-path degrees (<= kMaxRegDegree):
 // the cp.async ring (kernels_pipe.cu) or register loads (kernels_check/var.cu).
-// Measured on B200 (profiles/r1_kernel_choice.md): the ring wins for variable
-// nodes of degree >= 3, register loads for degree-2 variables and for checks.
+// Measured on B200 (profiles/r1_kernel_choice.md): the ring wins for every
+// variable bucket, register loads for checks (their slots are contiguous).
 // LDPC_KERNEL=reg|pipe forces one family (A/B runs).
 bool use_ring(bool var_side, int deg) {
     static const int forced = [] {
@@ -47,7 +47,7 @@ bool use_ring(bool var_side, int deg) {
         return 0;
     }();
     if (forced) return forced == 2;
-    return var_side && deg >= 3;
+    return var_side && deg >= 2;
 }
 
 size_t workspace_bytes(const ldpc_graph *g, int32_t B) {
@@ -67,6 +67,8 @@ int carve_workspace(const ldpc_graph *g, int32_t B, void *ws, size_t bytes, Work
     const size_t need = workspace_bytes(g, B);
     LDPC_ARG_CHECK(ws != nullptr && bytes >= need, "workspace too small: %zu < %zu bytes", bytes, need);
     LDPC_ARG_CHECK(((uintptr_t)ws & 255) == 0, "workspace must be 256-byte aligned");
+    LDPC_ARG_CHECK((uint64_t)g->E * 64 < (1ull << 32) && (uint64_t)g->n * 64 < (1ull << 32),
+                   "graph too large: %lld edges (32-bit row offsets need E < 2^26)", (long long)g->E);
     w->B = B;
     w->Bp = padded_batch(B);
     w->NW = w->Bp / 32;
@@ -485,21 +487,34 @@ extern "C" int ldpc_phase_f32(const ldpc_graph *g, int phase, const double *p_de
 // ---- host-buffer decoder: pipelined H2D / decode / D2H ------------------------
 // Device input and output buffers cover the whole max_batch, so every
 // sub-batch's H2D copy is enqueued up front on the copy stream (one event per
-// sub-batch) before the host spends time enqueuing decode launches; the compute
-// stream waits per sub-batch and the output stream returns each sub-batch's
-// packed results as soon as it is decoded.  Sub-batches grow geometrically
-// (64, 96, 144, ... up to `sub`) so the pipeline fill -- the first H2D, which
-// nothing overlaps -- stays short while later sub-batches are large enough to
-// run the kernels efficiently.
+// sub-batch) before the host spends time enqueuing decode launches; each
+// sub-batch waits for its own copy and the output stream returns its packed
+// results as soon as it is decoded.  Sub-batches grow geometrically (64, 96,
+// 144, ... up to `sub`) so the pipeline fill -- the first H2D, which nothing
+// overlaps -- stays short.  Consecutive sub-batches alternate between two
+// compute streams with their own workspaces, so a small sub-batch's kernel
+// tails are filled by the next one instead of idling SMs (a lone 64-codeword
+// decode runs ~20% below the full-batch rate).
 namespace {
 constexpr int kMaxChunks = 64;
+constexpr int kLanes = 2;
+int e2e_lanes() {
+    static const int v = [] {
+        const char *e = getenv("LDPC_E2E_LANES");
+        const int x = e ? atoi(e) : kLanes;
+        return x < 1 ? 1 : (x > kLanes ? kLanes : x);
+    }();
+    return v;
+}
 }
 
 struct ldpc_decoder {
     const ldpc_graph *g = nullptr;
     int32_t max_batch = 0, sub = 0;
-    cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
-    void *ws = nullptr;  // one workspace: decodes are serialised on s_comp
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaStream_t s_comp[kLanes] = {};  // sub-batch i decodes on s_comp[i % lanes] ...
+    void *ws[kLanes] = {};             // ... in workspace ws[i % lanes]
+    int lanes = 1;
     size_t ws_bytes = 0;
     double *p = nullptr;      // [max_batch][n]
     uint32_t *est = nullptr;  // [max_batch][RWn]
@@ -513,9 +528,9 @@ struct ldpc_decoder {
 
 static void decoder_free(ldpc_decoder *d) {
     if (!d) return;
-    for (cudaStream_t s : {d->s_in, d->s_comp, d->s_out})
+    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_out})
         if (s) cudaStreamSynchronize(s);
-    cudaFree(d->ws);
+    for (void *w : d->ws) cudaFree(w);
     cudaFree(d->p);
     cudaFree(d->est);
     cudaFree(d->syn);
@@ -524,7 +539,7 @@ static void decoder_free(ldpc_decoder *d) {
     for (int i = 0; i < kMaxChunks; i++)
         for (cudaEvent_t e : {d->in_ready[i], d->decoded[i]})
             if (e) cudaEventDestroy(e);
-    for (cudaStream_t s : {d->s_in, d->s_comp, d->s_out})
+    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_out})
         if (s) cudaStreamDestroy(s);
     delete d;
 }
@@ -557,9 +572,13 @@ extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32
     d->ws_bytes = workspace_bytes(g, biggest);
     const size_t RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32, MB = (size_t)max_batch;
     cudaError_t e = cudaSuccess;
-    for (cudaStream_t *s : {&d->s_in, &d->s_comp, &d->s_out})
+    d->lanes = chunk_plan(max_batch, d->sub).size() > 1 ? e2e_lanes() : 1;
+    for (cudaStream_t *s : {&d->s_in, &d->s_out})
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMalloc(&d->ws, d->ws_bytes);
+    for (int l = 0; l < d->lanes && e == cudaSuccess; l++) {
+        e = cudaStreamCreateWithFlags(&d->s_comp[l], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMalloc(&d->ws[l], d->ws_bytes);
+    }
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->p, sizeof(double) * (size_t)g->n * MB);
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->est, sizeof(uint32_t) * RWn * MB);
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->syn, sizeof(uint32_t) * RWm * MB);
@@ -612,12 +631,13 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
     // 2. decodes in order, each results copy right behind its decode
     for (size_t i = 0, c0 = 0; i < plan.size() && rc == LDPC_OK && e == cudaSuccess; c0 += plan[i], i++) {
         const int32_t b = plan[i];
-        cuda(cudaStreamWaitEvent(d->s_comp, d->in_ready[i], 0), "wait input");
+        const int l = (int)(i % d->lanes);
+        cuda(cudaStreamWaitEvent(d->s_comp[l], d->in_ready[i], 0), "wait input");
         if (e != cudaSuccess) break;
         rc = ldpc_decode(g, d->p + c0 * n, b, max_iterations, flags, d->est + c0 * RWn, d->succ + c0, d->its + c0,
-                         syn_bits_host ? d->syn + c0 * RWm : nullptr, d->ws, d->ws_bytes, d->s_comp, nullptr);
+                         syn_bits_host ? d->syn + c0 * RWm : nullptr, d->ws[l], d->ws_bytes, d->s_comp[l], nullptr);
         if (rc) break;
-        cuda(cudaEventRecord(d->decoded[i], d->s_comp), "record");
+        cuda(cudaEventRecord(d->decoded[i], d->s_comp[l]), "record");
         cuda(cudaStreamWaitEvent(d->s_out, d->decoded[i], 0), "wait decode");
         cuda(cudaMemcpyAsync(est_bits_host + c0 * RWn, d->est + c0 * RWn, sizeof(uint32_t) * RWn * b,
                              cudaMemcpyDeviceToHost, d->s_out), "D2H estimate");
@@ -628,7 +648,8 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
             cuda(cudaMemcpyAsync(syn_bits_host + c0 * RWm, d->syn + c0 * RWm, sizeof(uint32_t) * RWm * b,
                                  cudaMemcpyDeviceToHost, d->s_out), "D2H syndrome");
     }
-    for (cudaStream_t s : {d->s_in, d->s_comp, d->s_out}) cuda(cudaStreamSynchronize(s), "decode");
+    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_out})
+        if (s) cuda(cudaStreamSynchronize(s), "decode");
     if (rc == LDPC_OK && e != cudaSuccess) rc = LDPC_ECUDA;
     if (rc == LDPC_ECUDA) d->poisoned = true;  // mirrors engine.py:389-392: refuse further use
     return rc;

@@ -69,14 +69,14 @@ __device__ __forceinline__ bool chunk_done(const uint32_t *done, int chunk) {
 template <int D, int V, bool FROM_PRIOR>
 __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
     const int lane = threadIdx.x & 31;
-    const int chunks = a.Bp / (32 * V);
-    const int64_t task = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    // chunk-major sweep: all nodes of codeword chunk 0, then chunk 1, ...
-    const int ch = (int)(task / a.node_count);
-    const int ni = (int)(task - (int64_t)ch * a.node_count);
-    if (ch >= chunks) return;
+    // grid (node blocks, codeword chunks): blocks are dispatched x-fastest, so
+    // the grid sweeps all nodes of chunk 0, then chunk 1, ... (chunk-major)
+    const int ch = blockIdx.y;
+    const int ni = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (ni >= a.node_count) return;
     if (chunk_done<V>(a.done, ch)) return;
-    const int cw = ch * 32 * V + lane * V;
+    const int cw0 = ch * 32 * V;
+    double *mb = chunk_base(a.msg, a.msg_rows, cw0) + lane * V;
     // one round of independent index loads (bucket-ordered flat tables)
     const int32_t base = a.edge_begin + ni * D;
     int slot[D];
@@ -89,9 +89,10 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
         double q[V];
         if constexpr (FROM_PRIOR) {
             // pre-pass (serial.py:58,166): q = p[v-bar] straight from the priors
-            load_v_cached<V>(a.P + cofs(a.p_rows, __ldg(a.var_ord + base + i), cw), q);
+            const double *pb = chunk_base(a.P, a.p_rows, cw0) + lane * V;
+            load_v_cached<V>(pb + row_off(__ldg(a.var_ord + base + i)), q);
         } else {
-            load_v<V>(a.msg + cofs(a.msg_rows, slot[i], cw), q);
+            load_v<V>(mb + row_off(slot[i]), q);
         }
 #pragma unroll
         for (int v = 0; v < V; v++) b[i][v] = __dsub_rn(1.0, __dmul_rn(2.0, q[v]));
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
             for (int i = k + 1; i < D; i++) acc = __dmul_rn(acc, b[i][v]);
             out[v] = __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc)));
         }
-        store_v<V>(a.msg + cofs(a.msg_rows, slot[k], cw), out);
+        store_v<V>(mb + row_off(slot[k]), out);
         if (k + 1 < D) {
 #pragma unroll
             for (int v = 0; v < V; v++) pre[v] = __dmul_rn(pre[v], b[k][v]);
@@ -176,10 +177,10 @@ int vpolicy_check(int deg) {
 
 template <int D, int V, bool FP>
 int launch_one(const NodeLaunch &a, cudaStream_t s) {
-    const int64_t tasks = (int64_t)a.node_count * (a.Bp / (32 * V));
-    const int64_t blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    if (blocks == 0) return LDPC_OK;
-    k_check_reg<D, V, FP><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+    const dim3 grid((a.node_count + kWarpsPerBlock - 1) / kWarpsPerBlock, a.Bp / (32 * V));
+    if (a.node_count == 0) return LDPC_OK;
+    LDPC_ARG_CHECK(grid.y <= 65535u, "batch too large for one launch (%d codewords)", a.Bp);
+    k_check_reg<D, V, FP><<<grid, kThreads, 0, s>>>(a);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }

@@ -39,11 +39,33 @@ constexpr int ring_stages(int rows) {
     return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
+// Per stage: 32 row ids (one per lane), the task's codeword chunk at [32], pad to 16 bytes.
+constexpr int kIdsStride = 36;
 template <int ROWS, int V>
 struct Ring {
     static constexpr int S = ring_stages<V>(ROWS);
-    static constexpr size_t kIdsBytes = (size_t)S * 32 * sizeof(int);  // row ids per stage, one per lane
+    static constexpr size_t kIdsBytes = (size_t)S * kIdsStride * sizeof(int);
     static constexpr size_t kBytes = kIdsBytes + (size_t)S * ROWS * 32 * V * sizeof(double);
+};
+
+// The (chunk, node) of a warp's successive tasks t, t + W, t + 2W, ... (chunk-major
+// order t = ch * node_count + ni), advanced without a division per task.
+struct TaskCursor {
+    int ch, ni, dq, dr, nc;
+    __device__ __forceinline__ TaskCursor(int64_t t, int64_t W, int nc_) : nc(nc_) {
+        ch = (int)(t / nc);
+        ni = (int)(t - (int64_t)ch * nc);
+        dq = (int)(W / nc);
+        dr = (int)(W - (int64_t)dq * nc);
+    }
+    __device__ __forceinline__ void next() {
+        ni += dr;
+        ch += dq;
+        if (ni >= nc) {
+            ni -= nc;
+            ch += 1;
+        }
+    }
 };
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
@@ -90,8 +112,7 @@ __device__ __forceinline__ bool wchunk_done(const uint32_t *done, int ch) {
 //   variables: lane D = the variable (its prior row and c_hat row)
 //   checks FROM_PRIOR: lanes 16..16+D-1 = variables whose prior rows are the inputs
 template <int D, bool IS_VAR, bool FROM_PRIOR>
-__device__ __forceinline__ int load_id(const NodeLaunch &a, int64_t t, int lane) {
-    const int ni = (int)(t % a.node_count);
+__device__ __forceinline__ int load_id(const NodeLaunch &a, int ni, int lane) {
     const int32_t base = a.edge_begin + ni * D;
     if (lane < D) return __ldg(a.slot_ord + base + lane);
     if (IS_VAR && lane == D) return __ldg(a.order + a.node_begin + ni);
@@ -109,16 +130,19 @@ template <int D, bool IS_VAR>
 constexpr int ring_rows() { return D + (prior_in_ring<D, IS_VAR>() ? 1 : 0); }
 
 template <int D, int V, bool IS_VAR, bool FROM_PRIOR>
-__device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *ids_s, int64_t t, int id, int lane) {
+__device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *ids_s, int ch, int id, int lane) {
     constexpr int ROWS = ring_rows<D, IS_VAR>();
     constexpr int ROW = 32 * V;                 // doubles per row
     constexpr int RPI = V == 2 ? 1 : 2;         // rows per copy instruction
-    const int ch = (int)(t / a.node_count);
     ids_s[lane] = id;
+    if (lane == 0) ids_s[32] = ch;
     if (wchunk_done<V>(a.done, ch)) return;  // nothing to fetch; compute skips it too
     const int cw0 = ch * 32 * V;
     const int sub = V == 2 ? 0 : (lane >> 4);  // which row of the instruction's pair this lane copies
     const int piece = V == 2 ? lane : (lane & 15);
+    const double *mb = chunk_base(a.msg, a.msg_rows, cw0) + 2 * piece;
+    const double *pb = chunk_base(a.P, a.p_rows, cw0) + 2 * piece;
+    double *dst = rows + 2 * piece;
 #pragma unroll
     for (int j = 0; j < (ROWS + RPI - 1) / RPI; j++) {
         const int r = j * RPI + sub;
@@ -126,8 +150,8 @@ __device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *id
         const int rr = r < ROWS ? r : ROWS - 1;
         const bool prior_row = (prior_in_ring<D, IS_VAR>() && rr == D) || (!IS_VAR && FROM_PRIOR);
         const int src_id = __shfl_sync(0xffffffffu, id, (!IS_VAR && FROM_PRIOR) ? 16 + rr : rr);
-        const double *src = prior_row ? a.P + cofs(a.p_rows, src_id, cw0) : a.msg + cofs(a.msg_rows, src_id, cw0);
-        if (r < ROWS) cp_async16(rows + r * ROW + 2 * piece, src + 2 * piece);
+        const double *src = (prior_row ? pb : mb) + row_off(src_id);
+        if (r < ROWS) cp_async16(dst + r * ROW, src);
     }
 }
 
@@ -135,7 +159,7 @@ template <int D, int V>
 __device__ __forceinline__ void compute_check(const NodeLaunch &a, const double *rows, const int *ids, int ch,
                                               int lane) {
     constexpr int ROW = 32 * V;
-    const int cw = ch * 32 * V + lane * V;
+    double *mb = chunk_base(a.msg, a.msg_rows, ch * 32 * V) + lane * V;
     double b[D][V];
 #pragma unroll
     for (int i = 0; i < D; i++) {
@@ -157,7 +181,7 @@ __device__ __forceinline__ void compute_check(const NodeLaunch &a, const double 
             for (int i = k + 1; i < D; i++) acc = __dmul_rn(acc, b[i][v]);
             out[v] = __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc)));
         }
-        st_v<V>(a.msg + cofs(a.msg_rows, ids[k], cw), out);
+        st_v<V>(mb + row_off(ids[k]), out);
         if (k + 1 < D) {
 #pragma unroll
             for (int v = 0; v < V; v++) pre[v] = __dmul_rn(pre[v], b[k][v]);
@@ -169,7 +193,7 @@ template <int D, int V, bool WRITE_Q>
 __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *rows, const int *ids, int ch,
                                             int lane, const double (&pj)[V]) {
     constexpr int ROW = 32 * V;
-    const int cw = ch * 32 * V + lane * V;
+    double *mb = chunk_base(a.msg, a.msg_rows, ch * 32 * V) + lane * V;
     double r[D][V], om[D][V];
 #pragma unroll
     for (int i = 0; i < D; i++) {
@@ -201,7 +225,7 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
                 out[v] = ddiv_fast(q1, __dadd_rn(q0, q1), ok);  // den == 0 -> !ok
                 all_ok = all_ok && ok;
             }
-            if (all_ok) st_v<V>(a.msg + cofs(a.msg_rows, ids[k], cw), out);
+            if (all_ok) st_v<V>(mb + row_off(ids[k]), out);
             else slow |= 1u << k;
         }
 #pragma unroll
@@ -228,7 +252,7 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
                     const double den = __dadd_rn(q0, q1);
                     out[v] = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
                 }
-                st_v<V>(a.msg + cofs(a.msg_rows, ids[k], cw), out);
+                st_v<V>(mb + row_off(ids[k]), out);
             }
         }
     }
@@ -263,7 +287,7 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
 // a variable's prior row (V doubles per lane) straight into registers
 template <int V>
 __device__ __forceinline__ void load_prior(const NodeLaunch &a, int node, int ch, int lane, double (&o)[V]) {
-    const double *p = a.P + cofs(a.p_rows, node, ch * 32 * V + V * lane);
+    const double *p = chunk_base(a.P, a.p_rows, ch * 32 * V) + V * lane + row_off(node);
     if constexpr (V == 2) {
         const double2 x = __ldg(reinterpret_cast<const double2 *>(p));
         o[0] = x.x;
@@ -283,69 +307,97 @@ __global__ void __launch_bounds__(kThreads, V == 2 ? 2 : 3) k_node_ring(NodeLaun
     constexpr int S = R::S;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int *ids = reinterpret_cast<int *>(smem + (size_t)warp * R::kBytes);  // [S][32]
+    int *ids = reinterpret_cast<int *>(smem + (size_t)warp * R::kBytes);  // [S][kIdsStride]
     double *rows = reinterpret_cast<double *>(smem + (size_t)warp * R::kBytes + R::kIdsBytes);  // [S][ROWS][ROW]
     const int64_t W = (int64_t)gridDim.x * kWarpsPerBlock;
     const int64_t first = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+    if (first >= ntasks) return;
+    const int ntask = (int)((ntasks - first + W - 1) / W);  // this warp's tasks: first, first + W, ...
 
-    // prologue: ids of the first task, then copies of tasks 0..S-2 (one commit group per task)
-    int nid = first < ntasks ? load_id<D, IS_VAR, FP>(a, first, lane) : 0;
-    for (int s = 0; s < S - 1; s++) {
-        const int64_t t = first + s * W;
-        const int id = nid;
-        if (t + W < ntasks) nid = load_id<D, IS_VAR, FP>(a, t + W, lane);
-        if (t < ntasks) issue<D, V, IS_VAR, FP>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, t, id, lane);
+    // The row ids of task j are loaded two issues ahead (while task j - 2 is
+    // issued), so the index loads' L2 latency is off the critical path; the
+    // cursor runs two tasks ahead of the issue.
+    TaskCursor cur(first, W, a.node_count);
+    int nid0 = load_id<D, IS_VAR, FP>(a, cur.ni, lane), nch0 = cur.ch;
+    cur.next();
+    int nid1 = 0, nch1 = 0;
+    if (ntask > 1) {
+        nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
+        nch1 = cur.ch;
+        cur.next();
+    }
+    auto issue_next = [&](int j) {  // issue task j (j < ntask) into stage j % S
+        const int id = nid0, ich = nch0;
+        nid0 = nid1;
+        nch0 = nch1;
+        if (j + 2 < ntask) {
+            nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
+            nch1 = cur.ch;
+            cur.next();
+        }
+        const int sj = j % S;
+        issue<D, V, IS_VAR, FP>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, lane);
+    };
+    // prologue: copies of tasks 0..S-2 (one commit group per task)
+    for (int j = 0; j < S - 1; j++) {
+        if (j < ntask) issue_next(j);
         cp_commit();
     }
-    // variables: the prior row of the task being computed is loaded into registers
-    // one iteration ahead (it was issued S-1 >= 1 iterations ago, so its id is in smem)
-    double pnext[V] = {};
-    if (PREG && first < ntasks) {
+    // Variables of high degree: the prior row of a task is loaded into registers
+    // PD iterations before it is computed (its ids were issued S-1 >= PD
+    // iterations ahead, so they are in smem); one iteration did not cover the
+    // DRAM latency (ncu: the first use of the prior was the top stall).
+    constexpr int PD = S >= 3 ? 2 : 1;
+    double pq[PD][V] = {};
+    if (PREG) {
         __syncwarp();  // row ids written at issue (plain shared stores) are visible
-        load_prior<V>(a, ids[D], (int)(first / a.node_count), lane, pnext);
+#pragma unroll
+        for (int d = 0; d < PD; d++)
+            if (d < ntask) load_prior<V>(a, ids[d * kIdsStride + D], ids[d * kIdsStride + 32], lane, pq[d]);
     }
-    int it = 0;
-    for (int64_t t = first; t < ntasks; t += W, it++) {
-        // keep S-1 tasks in flight: issue task t + (S-1) W into the stage freed last iteration
-        const int64_t tn = t + (int64_t)(S - 1) * W;
-        const int sn = (it + S - 1) % S;
-        const int id = nid;
-        if (tn + W < ntasks) nid = load_id<D, IS_VAR, FP>(a, tn + W, lane);
-        if (tn < ntasks) issue<D, V, IS_VAR, FP>(a, rows + (size_t)sn * ROWS * ROW, ids + sn * 32, tn, id, lane);
+    for (int it = 0; it < ntask; it++) {
+        // keep S-1 tasks in flight: issue task it + S-1 into the stage freed last iteration
+        if (it + S - 1 < ntask) issue_next(it + S - 1);
         cp_commit();
-        cp_wait<S - 1>();  // this lane's copies of task t have landed
+        cp_wait<S - 1>();  // this lane's copies of task it have landed
         __syncwarp();      // ... and every other lane's (V=1 lanes read pieces copied by other lanes)
         const int s = it % S;
-        const int ch = (int)(t / a.node_count);
+        const int *ids_s = ids + s * kIdsStride;
+        const int ch = ids_s[32];
         double pj[V];
         if constexpr (PREG) {
 #pragma unroll
-            for (int v = 0; v < V; v++) pj[v] = pnext[v];
+            for (int v = 0; v < V; v++) pj[v] = pq[0][v];
+#pragma unroll
+            for (int d = 0; d + 1 < PD; d++)
+#pragma unroll
+                for (int v = 0; v < V; v++) pq[d][v] = pq[d + 1][v];
+            if (it + PD < ntask) {
+                const int *idsn = ids + ((it + PD) % S) * kIdsStride;
+                load_prior<V>(a, idsn[D], idsn[32], lane, pq[PD - 1]);
+            }
         } else if constexpr (IS_VAR) {
             ld_smem<V>(rows + (size_t)s * ROWS * ROW + D * ROW + V * lane, pj);
         }
-        if (PREG && t + W < ntasks) {
-            const int s1 = (it + 1) % S;  // task t + W was issued at least one iteration ago
-            load_prior<V>(a, ids[s1 * 32 + D], (int)((t + W) / a.node_count), lane, pnext);
-        }
         if (!wchunk_done<V>(a.done, ch)) {
-            if constexpr (IS_VAR) compute_var<D, V, FLAG>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, ch, lane, pj);
-            else compute_check<D, V>(a, rows + (size_t)s * ROWS * ROW, ids + s * 32, ch, lane);
+            if constexpr (IS_VAR) compute_var<D, V, FLAG>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane, pj);
+            else compute_check<D, V>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane);
         }
         __syncwarp();  // stage s is reused by the issue of the next iteration
     }
     cp_wait<0>();
 }
 
+// Codewords per lane: V=1 (3 blocks/SM, more warps to hide the fp64 chains) for
+// variables of degree >= 3, V=2 (16-byte rows pieces per lane) for degree 2 and
+// checks (profiles/r1_kernel_choice.md).  LDPC_RING_V=1|2 forces one.
 int ring_v(bool var_side, int deg) {
     static const int forced = [] {
         const char *e = getenv("LDPC_RING_V");
         return e ? atoi(e) : 0;
     }();
     if (forced == 1 || forced == 2) return forced;
-    (void)var_side;
-    (void)deg;
-    return 2;  // V=1 measured slower for every bucket (profiles/r1_kernel_choice.md)
+    return var_side && deg >= 3 ? 1 : 2;
 }
 
 template <int D, int V, bool IS_VAR, bool FLAG>

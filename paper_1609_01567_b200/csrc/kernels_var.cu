@@ -65,12 +65,10 @@ __device__ __forceinline__ void put_bits(uint32_t *dst, uint32_t bits, const uin
 template <int D, int V, bool WRITE_Q>
 __global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_reg(NodeLaunch a) {
     const int lane = threadIdx.x & 31;
-    const int chunks = a.Bp / (32 * V);
-    const int64_t task = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    // chunk-major sweep: all nodes of codeword chunk 0, then chunk 1, ...
-    const int ch = (int)(task / a.node_count);
-    const int ni = (int)(task - (int64_t)ch * a.node_count);
-    if (ch >= chunks) return;
+    // grid (node blocks, codeword chunks), dispatched x-fastest: chunk-major sweep
+    const int ch = blockIdx.y;
+    const int ni = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (ni >= a.node_count) return;
     if (a.done != nullptr) {
         bool all;
         if constexpr (V == 2) {
@@ -81,7 +79,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_re
         }
         if (all) return;
     }
-    const int cw = ch * 32 * V + lane * V;
+    const int cw0 = ch * 32 * V;
+    double *mb = chunk_base(a.msg, a.msg_rows, cw0) + lane * V;
     // one round of independent index loads (bucket-ordered flat tables)
     const int node = __ldg(a.order + a.node_begin + ni);
     const int32_t base = a.edge_begin + ni * D;
@@ -90,10 +89,10 @@ __global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_re
     for (int i = 0; i < D; i++) pos[i] = __ldg(a.slot_ord + base + i);
 
     double pj[V];
-    load_prior<V>(a.P + cofs(a.p_rows, node, cw), pj);
+    load_prior<V>(chunk_base(a.P, a.p_rows, cw0) + lane * V + row_off(node), pj);
     double r[D][V];
 #pragma unroll
-    for (int i = 0; i < D; i++) load_v<V>(a.msg + cofs(a.msg_rows, pos[i], cw), r[i]);
+    for (int i = 0; i < D; i++) load_v<V>(mb + row_off(pos[i]), r[i]);
     double om[D][V];  // 1 - r_i
 #pragma unroll
     for (int i = 0; i < D; i++)
@@ -124,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_re
                 out[v] = ddiv_fast(q1, __dadd_rn(q0, q1), ok);  // den == 0 -> !ok
                 all_ok = all_ok && ok;
             }
-            if (all_ok) store_v<V>(a.msg + cofs(a.msg_rows, pos[k], cw), out);
+            if (all_ok) store_v<V>(mb + row_off(pos[k]), out);
             else slow |= 1u << k;
         }
 #pragma unroll
@@ -149,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_re
                     const double den = __dadd_rn(q0, q1);
                     out[v] = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
                 }
-                store_v<V>(a.msg + cofs(a.msg_rows, pos[k], cw), out);
+                store_v<V>(mb + row_off(pos[k]), out);
             }
         }
     }
@@ -260,10 +259,10 @@ int vpolicy_var(int deg) {
 
 template <int D, int V, bool WQ>
 int launch_one(const NodeLaunch &a, cudaStream_t s) {
-    const int64_t tasks = (int64_t)a.node_count * (a.Bp / (32 * V));
-    const int64_t blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    if (blocks == 0) return LDPC_OK;
-    k_var_reg<D, V, WQ><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+    const dim3 grid((a.node_count + kWarpsPerBlock - 1) / kWarpsPerBlock, a.Bp / (32 * V));
+    if (a.node_count == 0) return LDPC_OK;
+    LDPC_ARG_CHECK(grid.y <= 65535u, "batch too large for one launch (%d codewords)", a.Bp);
+    k_var_reg<D, V, WQ><<<grid, kThreads, 0, s>>>(a);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }
