@@ -72,6 +72,7 @@ int carve_workspace(const ldpc_graph *g, int32_t B, void *ws, size_t bytes, Work
     w->B = B;
     w->Bp = padded_batch(B);
     w->NW = w->Bp / 32;
+    w->NWs = w->NW;
     char *p = (char *)ws;
     auto take = [&](size_t sz) {
         char *r = p;
@@ -86,6 +87,25 @@ int carve_workspace(const ldpc_graph *g, int32_t B, void *ws, size_t bytes, Work
     w->unsat = (uint32_t *)take(sizeof(uint32_t) * w->NW);
     w->iters = (int32_t *)take(sizeof(int32_t) * w->Bp);
     return LDPC_OK;
+}
+
+Workspace tile_view(const ldpc_graph *g, const Workspace &w, int32_t group0, int32_t groups) {
+    // groups of 32 codewords; a multi-group view must start on a 64-codeword chunk so the
+    // chunk arithmetic of the kernels (relative to the view base) stays valid
+    Workspace v = w;
+    const size_t chunk = (size_t)(group0 >> 1), half = (size_t)(group0 & 1) * 32;
+    v.msg = w.msg + chunk * (size_t)g->E * 64 + half;
+    v.P = w.P + chunk * (size_t)g->n * 64 + half;
+    v.chat = w.chat + group0;
+    v.zb = w.zb + group0;
+    v.done = w.done + group0;
+    v.unsat = w.unsat + group0;
+    v.iters = w.iters + 32 * (size_t)group0;
+    v.Bp = 32 * groups;
+    v.B = std::max(0, std::min(w.B - 32 * group0, v.Bp));
+    v.NW = groups;
+    v.NWs = w.NWs;
+    return v;
 }
 
 namespace {
@@ -150,12 +170,12 @@ struct Prof {
     } while (0)
 
 NodeLaunch check_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
-    return NodeLaunch{g->chk_off, g->chk_var, g->chk_order, 0, 0, w.msg, w.P, nullptr, done, w.Bp, w.NW,
+    return NodeLaunch{g->chk_off, g->chk_var, g->chk_order, 0, 0, w.msg, w.P, nullptr, done, w.Bp, w.NWs,
                       (int32_t)g->E, g->n, g->chk_slot, g->chk_slot_ord, g->chk_var_ord, 0};
 }
 
 NodeLaunch var_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
-    return NodeLaunch{g->var_off, nullptr, g->var_order, 0, 0, w.msg, w.P, w.chat, done, w.Bp, w.NW,
+    return NodeLaunch{g->var_off, nullptr, g->var_order, 0, 0, w.msg, w.P, w.chat, done, w.Bp, w.NWs,
                       (int32_t)g->E, g->n, g->var_slot, g->var_slot_ord, nullptr, 0};
 }
 
@@ -255,21 +275,16 @@ int init_flags(const Workspace &w, bool early, cudaStream_t s) {
 
 }  // namespace
 
-// The decode proper on a carved workspace whose P is filled.
-int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s, Prof &prof,
-               bool fast = false) {
+// Algorithm 2 (serial.py:165-178) on one view of the workspace: the whole batch
+// (streaming schedule) or one tile (tiled schedule).
+static int decode_view(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s,
+                       Prof &prof, bool fast) {
     const int64_t B = w.B, E = g->E, n = g->n, m = g->m;
     const int64_t wb = fast ? 4 : 8;                         // message / prior width in bytes
     const int64_t c_bytes = 2 * wb * E * B;                  // read q (or p-gather) + write r
     const int64_t ve_bytes = (2 * wb * E + wb * n + n / 8) * B; // read r, p; write q, c_hat bits
     const int64_t e_bytes = (wb * E + wb * n + n / 8) * B;   // read r, p; write c_hat bits
     const int64_t s_bytes = (n / 8) * B;                     // read c_hat bits
-    int rc = init_flags(w, early, s);
-    if (rc) return rc;
-    if (fast) {
-        rc = launch_priors_to_f32(w.P, prior32(g, w), (size_t)g->n * w.Bp, s);
-        if (rc) return rc;
-    }
     const uint32_t *done = early ? w.done : nullptr;
     RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, true, nullptr, s, fast));
     for (int32_t t = 1; t <= max_iter; t++) {
@@ -283,7 +298,49 @@ int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool e
     RUN(LDPC_KCLASS_ESTIMATE, e_bytes, var_phase(g, w, false, done, s, fast));
     RUN(LDPC_KCLASS_SYNDROME, s_bytes + (m / 8) * B, launch_syndrome(g, w, true, early, s));
     if (early) RUN(LDPC_KCLASS_SYNDROME, 0, launch_update_done(w, max_iter, true, s));
-    (void)m;
+    return LDPC_OK;
+}
+
+// Tiled (L2-resident) schedule, OFF by default: instead of sweeping every phase
+// over the whole batch (each half-iteration one HBM round trip of the 1.86 GB
+// message array at C3), run ALL iterations of one tile of codewords before the
+// next, the tile's messages + priors sized to stay in the 126 MB L2.  Codewords
+// are independent, so results are bit-identical to the streaming schedule.
+// Measured on B200 (profiles/r1_kernel_choice.md): pure data movement gains
+// 1.33x in this pattern, but the node kernels become issue-bound on a 32-codeword
+// tile (the deg-8 variable kernel needs ~4.8 us of instruction issue per tile at
+// IPC 1 vs 6.3 us of L2 traffic), so C3 runs at 18.8 ms tiled vs 14.2 ms
+// streaming.  Kept as an experiment switch: LDPC_TILE=k runs tiles of k
+// 32-codeword groups (even when >= 2 so views stay chunk-aligned).
+static int32_t tile_groups(const ldpc_graph *g, const Workspace &w, bool fast) {
+    static const int forced = [] {
+        const char *e = getenv("LDPC_TILE");
+        return e ? atoi(e) : 0;
+    }();
+    (void)g;
+    if (fast || forced <= 0) return 0;
+    const int32_t groups = (w.B + 31) / 32;
+    int32_t T = forced;
+    if (T >= 2) T &= ~1;
+    return std::min(T, groups);
+}
+
+// The decode proper on a carved workspace whose P is filled.
+int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s, Prof &prof,
+               bool fast = false) {
+    int rc = init_flags(w, early, s);
+    if (rc) return rc;
+    if (fast) {
+        rc = launch_priors_to_f32(w.P, prior32(g, w), (size_t)g->n * w.Bp, s);
+        if (rc) return rc;
+    }
+    const int32_t T = tile_groups(g, w, fast);
+    if (T == 0) return decode_view(g, w, max_iter, early, s, prof, fast);
+    const int32_t groups = (w.B + 31) / 32;
+    for (int32_t g0 = 0; g0 < groups; g0 += T) {
+        rc = decode_view(g, tile_view(g, w, g0, std::min(T, groups - g0)), max_iter, early, s, prof, fast);
+        if (rc) return rc;
+    }
     return LDPC_OK;
 }
 

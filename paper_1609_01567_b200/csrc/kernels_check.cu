@@ -26,11 +26,11 @@ namespace {
 template <int V>
 __device__ __forceinline__ void load_v(const double *p, double (&o)[V]) {
     if constexpr (V == 2) {
-        double2 t = __ldcs(reinterpret_cast<const double2 *>(p));
+        double2 t = ld_msg(reinterpret_cast<const double2 *>(p));
         o[0] = t.x;
         o[1] = t.y;
     } else {
-        o[0] = __ldcs(p);
+        o[0] = ld_msg(p);
     }
 }
 
@@ -48,9 +48,9 @@ __device__ __forceinline__ void load_v_cached(const double *p, double (&o)[V]) {
 template <int V>
 __device__ __forceinline__ void store_v(double *p, const double (&o)[V]) {
     if constexpr (V == 2) {
-        __stcs(reinterpret_cast<double2 *>(p), make_double2(o[0], o[1]));
+        st_msg(reinterpret_cast<double2 *>(p), make_double2(o[0], o[1]));
     } else {
-        __stcs(p, o[0]);
+        st_msg(p, o[0]);
     }
 }
 
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) k_check_wide(NodeLaunch a, int TW, i
     const int d = __ldg(a.off + node + 1) - pos0;
     for (int i = worker; i < d; i += nwk) {
         double q = FROM_PRIOR ? __ldg(a.P + cofs(a.p_rows, __ldg(a.idx + pos0 + i), cw))
-                              : __ldcs(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + i) : pos0 + i, cw));
+                              : ld_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + i) : pos0 + i, cw));
         b[i * TW + c] = __dsub_rn(1.0, __dmul_rn(2.0, q));
     }
     __syncthreads();
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads) k_check_wide(NodeLaunch a, int TW, i
         const int k = (j & 1) ? (d - 1 - (j >> 1)) : (j >> 1);
         double acc = pre[k * TW + c];
         for (int i = k + 1; i < d; i++) acc = __dmul_rn(acc, b[i * TW + c]);
-        __stcs(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + k) : pos0 + k, cw), __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc))));
+        st_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + k) : pos0 + k, cw), __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc))));
     }
 }
 
@@ -187,7 +187,7 @@ int launch_one(const NodeLaunch &a, cudaStream_t s) {
 
 template <int D>
 int launch_deg(const NodeLaunch &a, bool fp, cudaStream_t s) {
-    const int V = vpolicy_check(D);
+    const int V = (a.Bp % 64) ? 1 : vpolicy_check(D);  // tile views of 32 codewords take V=1
     if (V == 2) return fp ? launch_one<D, 2, true>(a, s) : launch_one<D, 2, false>(a, s);
     return fp ? launch_one<D, 1, true>(a, s) : launch_one<D, 1, false>(a, s);
 }

@@ -37,7 +37,7 @@ __global__ void k_transpose_priors(const double *__restrict__ in, int32_t B, int
 
 // blockDim (32, 8): x -> word, y -> check; grid (check slabs, word groups)
 __global__ void k_syndrome(const int32_t *__restrict__ chk_off, const int32_t *__restrict__ chk_var, int32_t m,
-                           const uint32_t *__restrict__ chat, int32_t NW, uint32_t *__restrict__ zb,
+                           const uint32_t *__restrict__ chat, int32_t NW, int32_t NWs, uint32_t *__restrict__ zb,
                            uint32_t *__restrict__ unsat, const uint32_t *__restrict__ done) {
     __shared__ uint32_t red[8][32];
     const int w = blockIdx.y * 32 + threadIdx.x;
@@ -47,12 +47,12 @@ __global__ void k_syndrome(const int32_t *__restrict__ chk_off, const int32_t *_
         for (int i = blockIdx.x * 8 + threadIdx.y; i < m; i += gridDim.x * 8) {
             const int a = __ldg(chk_off + i), b = __ldg(chk_off + i + 1);
             uint32_t z = 0;
-            for (int p = a; p < b; p++) z ^= chat[(size_t)__ldg(chk_var + p) * NW + w];
-            if (zb != nullptr) zb[(size_t)i * NW + w] = z;
+            for (int p = a; p < b; p++) z ^= chat[(size_t)__ldg(chk_var + p) * NWs + w];
+            if (zb != nullptr) zb[(size_t)i * NWs + w] = z;
             acc |= z;
         }
     } else if (w < NW && zb != nullptr) {
-        for (int i = blockIdx.x * 8 + threadIdx.y; i < m; i += gridDim.x * 8) zb[(size_t)i * NW + w] = 0;
+        for (int i = blockIdx.x * 8 + threadIdx.y; i < m; i += gridDim.x * 8) zb[(size_t)i * NWs + w] = 0;
     }
     red[threadIdx.y][threadIdx.x] = acc;
     __syncthreads();
@@ -211,7 +211,7 @@ int launch_transpose_priors(const double *p_in, int32_t B, int32_t n, double *P,
 int launch_syndrome(const ldpc_graph *g, const Workspace &w, bool write_z, bool use_done, cudaStream_t s) {
     const unsigned gx = blocks_for(g->m, 8, 148 * 8);
     dim3 grid(gx, (w.NW + 31) / 32);
-    k_syndrome<<<grid, dim3(32, 8), 0, s>>>(g->chk_off, g->chk_var, g->m, w.chat, w.NW, write_z ? w.zb : nullptr,
+    k_syndrome<<<grid, dim3(32, 8), 0, s>>>(g->chk_off, g->chk_var, g->m, w.chat, w.NW, w.NWs, write_z ? w.zb : nullptr,
                                              w.unsat, use_done ? w.done : nullptr);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;

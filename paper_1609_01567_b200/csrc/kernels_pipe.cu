@@ -80,8 +80,8 @@ __device__ __forceinline__ void cp_wait() {
 
 template <int V>
 __device__ __forceinline__ void st_v(double *p, const double (&o)[V]) {
-    if constexpr (V == 2) __stcs(reinterpret_cast<double2 *>(p), make_double2(o[0], o[1]));
-    else __stcs(p, o[0]);
+    if constexpr (V == 2) st_msg(reinterpret_cast<double2 *>(p), make_double2(o[0], o[1]));
+    else st_msg(p, o[0]);
 }
 
 template <int V>
@@ -434,7 +434,7 @@ int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
 
 template <int D, bool IS_VAR, bool FLAG>
 int launch_ring(const NodeLaunch &a, cudaStream_t st) {
-    return ring_v(IS_VAR, D) == 1 ? launch_ring_v<D, 1, IS_VAR, FLAG>(a, st) : launch_ring_v<D, 2, IS_VAR, FLAG>(a, st);
+    return (a.Bp % 64 || ring_v(IS_VAR, D) == 1) ? launch_ring_v<D, 1, IS_VAR, FLAG>(a, st) : launch_ring_v<D, 2, IS_VAR, FLAG>(a, st);
 }
 
 }  // namespace

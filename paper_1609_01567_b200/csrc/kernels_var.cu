@@ -25,11 +25,11 @@ namespace {
 template <int V>
 __device__ __forceinline__ void load_v(const double *p, double (&o)[V]) {
     if constexpr (V == 2) {
-        double2 t = __ldcs(reinterpret_cast<const double2 *>(p));
+        double2 t = ld_msg(reinterpret_cast<const double2 *>(p));
         o[0] = t.x;
         o[1] = t.y;
     } else {
-        o[0] = __ldcs(p);
+        o[0] = ld_msg(p);
     }
 }
 
@@ -47,9 +47,9 @@ __device__ __forceinline__ void load_prior(const double *p, double (&o)[V]) {
 template <int V>
 __device__ __forceinline__ void store_v(double *p, const double (&o)[V]) {
     if constexpr (V == 2) {
-        __stcs(reinterpret_cast<double2 *>(p), make_double2(o[0], o[1]));
+        st_msg(reinterpret_cast<double2 *>(p), make_double2(o[0], o[1]));
     } else {
-        __stcs(p, o[0]);
+        st_msg(p, o[0]);
     }
 }
 
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kThreads) k_var_wide(NodeLaunch a, int TW, int
     const int d = __ldg(a.off + node + 1) - e0;
     for (int i = threadIdx.x; i < d; i += blockDim.x) spos[i] = a.slot ? __ldg(a.slot + e0 + i) : e0 + i;
     __syncthreads();
-    for (int i = worker; i < d; i += nwk) r[i * TW + c] = __ldcs(a.msg + cofs(a.msg_rows, spos[i], cw));
+    for (int i = worker; i < d; i += nwk) r[i * TW + c] = ld_msg(a.msg + cofs(a.msg_rows, spos[i], cw));
     __syncthreads();
     if (worker == 0) {
         const double p = __ldg(a.P + cofs(a.p_rows, node, cw));
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_var_wide(NodeLaunch a, int TW, int
             bool ok;
             double q = ddiv_fast(q1, den, ok);
             if (!ok) q = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
-            __stcs(a.msg + cofs(a.msg_rows, spos[k], cw), q);
+            st_msg(a.msg + cofs(a.msg_rows, spos[k], cw), q);
         }
     }
     if (worker == 0) {
@@ -269,7 +269,7 @@ int launch_one(const NodeLaunch &a, cudaStream_t s) {
 
 template <int D>
 int launch_deg(const NodeLaunch &a, bool wq, cudaStream_t s) {
-    const int V = vpolicy_var(D);
+    const int V = (a.Bp % 64) ? 1 : vpolicy_var(D);  // tile views of 32 codewords take V=1
     if (V == 2) return wq ? launch_one<D, 2, true>(a, s) : launch_one<D, 2, false>(a, s);
     return wq ? launch_one<D, 1, true>(a, s) : launch_one<D, 1, false>(a, s);
 }
