@@ -74,6 +74,8 @@ def _declare(L):
     L.ldpc_phase_syndrome.argtypes = [vp, vp, vp, i32, vp, sz, vp]
     L.ldpc_decoder_create.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.ldpc_decoder_decode_host.argtypes = [vp, vp, i32, i32, u32, vp, vp, vp, vp]
+    L.ldpc_decoder_submit.argtypes = [vp, vp, i32, i32, u32, vp, vp, vp, vp, P_i64]
+    L.ldpc_decoder_wait.argtypes = [vp, i64]
     L.ldpc_decoder_destroy.argtypes = [vp]
     L.ldpc_decoder_destroy.restype = None
     u64 = ctypes.c_uint64
@@ -88,7 +90,7 @@ def _declare(L):
     for name in ("ldpc_graph_create", "ldpc_graph_info", "ldpc_graph_get_tables", "ldpc_graph_get_var_groups",
                  "ldpc_graph_get_buckets", "ldpc_decode", "ldpc_count_errors", "ldpc_phase_to_check",
                  "ldpc_phase_to_variable", "ldpc_phase_estimate", "ldpc_phase_syndrome", "ldpc_decoder_create",
-                 "ldpc_decoder_decode_host"):
+                 "ldpc_decoder_decode_host", "ldpc_decoder_submit", "ldpc_decoder_wait"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

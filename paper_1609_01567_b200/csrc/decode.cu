@@ -579,6 +579,18 @@ struct ldpc_decoder {
     uint8_t *succ = nullptr;  // [max_batch]
     int32_t *its = nullptr;   // [max_batch]
     cudaEvent_t in_ready[kMaxChunks] = {}, decoded[kMaxChunks] = {};
+    // streaming slots (ldpc_decoder_submit / wait), allocated on first use
+    struct Slot {
+        double *p = nullptr;
+        uint32_t *est = nullptr, *syn = nullptr;
+        uint8_t *succ = nullptr;
+        int32_t *its = nullptr;
+        cudaEvent_t in_done = nullptr, dec_done = nullptr, out_done = nullptr;
+        int64_t ticket = -1;  // in flight when >= 0
+    } slots[2];
+    void *ws_full = nullptr;  // workspace for a whole max_batch decode
+    size_t ws_full_bytes = 0;
+    int64_t next_ticket = 0;
     bool poisoned = false;
     std::mutex mu;
 };
@@ -588,6 +600,16 @@ static void decoder_free(ldpc_decoder *d) {
     for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_out})
         if (s) cudaStreamSynchronize(s);
     for (void *w : d->ws) cudaFree(w);
+    cudaFree(d->ws_full);
+    for (auto &sl : d->slots) {
+        cudaFree(sl.p);
+        cudaFree(sl.est);
+        cudaFree(sl.syn);
+        cudaFree(sl.succ);
+        cudaFree(sl.its);
+        for (cudaEvent_t e : {sl.in_done, sl.dec_done, sl.out_done})
+            if (e) cudaEventDestroy(e);
+    }
     cudaFree(d->p);
     cudaFree(d->est);
     cudaFree(d->syn);
@@ -710,6 +732,116 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
     if (rc == LDPC_OK && e != cudaSuccess) rc = LDPC_ECUDA;
     if (rc == LDPC_ECUDA) d->poisoned = true;  // mirrors engine.py:389-392: refuse further use
     return rc;
+}
+
+// ---- streaming: submit / wait ---------------------------------------------------
+static int slot_finish(ldpc_decoder *d, ldpc_decoder::Slot &sl) {
+    if (sl.ticket < 0) return LDPC_OK;
+    const cudaError_t e = cudaEventSynchronize(sl.out_done);
+    sl.ticket = -1;
+    if (e != cudaSuccess) {
+        set_error("decode: %s", cudaGetErrorString(e));
+        d->poisoned = true;
+        return LDPC_ECUDA;
+    }
+    return LDPC_OK;
+}
+
+static int slots_alloc(ldpc_decoder *d) {
+    if (d->slots[0].p != nullptr) return LDPC_OK;
+    const ldpc_graph *g = d->g;
+    const size_t RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32, MB = (size_t)d->max_batch;
+    cudaError_t e = cudaSuccess;
+    d->ws_full_bytes = workspace_bytes(g, d->max_batch);
+    e = cudaMalloc(&d->ws_full, d->ws_full_bytes);
+    for (auto &sl : d->slots) {
+        if (e == cudaSuccess) e = cudaMalloc((void **)&sl.p, sizeof(double) * (size_t)g->n * MB);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&sl.est, sizeof(uint32_t) * RWn * MB);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&sl.syn, sizeof(uint32_t) * RWm * MB);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&sl.succ, MB);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&sl.its, sizeof(int32_t) * MB);
+        for (cudaEvent_t *ev : {&sl.in_done, &sl.dec_done, &sl.out_done})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        set_error("streaming slots: %s", cudaGetErrorString(e));
+        cudaGetLastError();
+        return e == cudaErrorMemoryAllocation ? LDPC_ENOMEM : LDPC_ECUDA;
+    }
+    return LDPC_OK;
+}
+
+extern "C" int ldpc_decoder_submit(ldpc_decoder *d, const double *p_host, int32_t B, int32_t max_iterations,
+                                   uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
+                                   int32_t *iters_host, uint32_t *syn_bits_host, int64_t *ticket) {
+    if (d == nullptr) {
+        set_error("decoder is closed");
+        return LDPC_ECLOSED;
+    }
+    std::lock_guard<std::mutex> lock(d->mu);
+    if (d->poisoned) {
+        set_error("decoder is closed after a device fault");
+        return LDPC_ECLOSED;
+    }
+    LDPC_ARG_CHECK(p_host && est_bits_host && success_host && iters_host && ticket, "NULL argument");
+    LDPC_ARG_CHECK(B >= 1 && B <= d->max_batch, "batch %d outside 1..%d", B, d->max_batch);
+    LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
+    int rc = slots_alloc(d);
+    if (rc) return rc;
+    const int64_t k = d->next_ticket;
+    auto &sl = d->slots[k & 1];
+    if ((rc = slot_finish(d, sl))) return rc;  // the slot's previous batch (ticket k - 2) is home
+    const ldpc_graph *g = d->g;
+    const size_t n = g->n, RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32;
+    cudaStream_t sc = d->s_comp[0];
+    cudaError_t e = cudaSuccess;
+    auto cuda = [&](cudaError_t x, const char *what) {
+        if (x != cudaSuccess && e == cudaSuccess) {
+            e = x;
+            set_error("%s: %s", what, cudaGetErrorString(x));
+        }
+    };
+    cuda(cudaMemcpyAsync(sl.p, p_host, sizeof(double) * n * B, cudaMemcpyHostToDevice, d->s_in), "H2D priors");
+    cuda(cudaEventRecord(sl.in_done, d->s_in), "record");
+    cuda(cudaStreamWaitEvent(sc, sl.in_done, 0), "wait input");
+    if (e == cudaSuccess)
+        rc = ldpc_decode(g, sl.p, B, max_iterations, flags, sl.est, sl.succ, sl.its,
+                         syn_bits_host ? sl.syn : nullptr, d->ws_full, d->ws_full_bytes, sc, nullptr);
+    if (rc == LDPC_OK && e == cudaSuccess) {
+        cuda(cudaEventRecord(sl.dec_done, sc), "record");
+        cuda(cudaStreamWaitEvent(d->s_out, sl.dec_done, 0), "wait decode");
+        cuda(cudaMemcpyAsync(est_bits_host, sl.est, sizeof(uint32_t) * RWn * B, cudaMemcpyDeviceToHost, d->s_out),
+             "D2H estimate");
+        cuda(cudaMemcpyAsync(success_host, sl.succ, B, cudaMemcpyDeviceToHost, d->s_out), "D2H success");
+        cuda(cudaMemcpyAsync(iters_host, sl.its, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, d->s_out),
+             "D2H iterations");
+        if (syn_bits_host)
+            cuda(cudaMemcpyAsync(syn_bits_host, sl.syn, sizeof(uint32_t) * RWm * B, cudaMemcpyDeviceToHost,
+                                 d->s_out), "D2H syndrome");
+        cuda(cudaEventRecord(sl.out_done, d->s_out), "record");
+    }
+    if (rc == LDPC_OK && e != cudaSuccess) rc = LDPC_ECUDA;
+    if (rc == LDPC_ECUDA) {
+        d->poisoned = true;
+        return rc;
+    }
+    if (rc) return rc;
+    sl.ticket = k;
+    d->next_ticket = k + 1;
+    *ticket = k;
+    return LDPC_OK;
+}
+
+extern "C" int ldpc_decoder_wait(ldpc_decoder *d, int64_t ticket) {
+    if (d == nullptr) {
+        set_error("decoder is closed");
+        return LDPC_ECLOSED;
+    }
+    std::lock_guard<std::mutex> lock(d->mu);
+    LDPC_ARG_CHECK(ticket >= 0 && ticket < d->next_ticket, "unknown ticket %lld", (long long)ticket);
+    auto &sl = d->slots[ticket & 1];
+    if (sl.ticket != ticket) return d->poisoned ? LDPC_ECLOSED : LDPC_OK;  // already collected
+    return slot_finish(d, sl);
 }
 
 extern "C" void ldpc_decoder_destroy(ldpc_decoder *d) { decoder_free(d); }

@@ -31,19 +31,20 @@ namespace {
 // V = codewords per lane (1 or 2): a task is (node, 32*V codewords), a row is
 // 32*V doubles (256*V bytes).  Copies are always 16 bytes per lane, so a V=1
 // warp moves two rows per cp.async instruction.
-// ring depth from a per-warp budget (~13 KB at 16 warps/SM for V=2, ~9 KB at 24 warps/SM for V=1)
-template <int V>
+// ring depth from a per-warp shared-memory budget at MINB resident blocks (8 warps each) per SM:
+// ~13 KB at 2 blocks, ~9 KB at 3, ~6.5 KB at 4
+template <int V, int MINB>
 constexpr int ring_stages(int rows) {
-    const int budget = V == 2 ? 13 * 1024 : 9 * 1024;
+    const int budget = MINB <= 2 ? 13 * 1024 : (MINB == 3 ? 9 * 1024 : 6656);
     const int s = budget / (rows * 32 * V * 8);
     return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
 // Per stage: 32 row ids (one per lane), the task's codeword chunk at [32], pad to 16 bytes.
 constexpr int kIdsStride = 36;
-template <int ROWS, int V>
+template <int ROWS, int V, int MINB>
 struct Ring {
-    static constexpr int S = ring_stages<V>(ROWS);
+    static constexpr int S = ring_stages<V, MINB>(ROWS);
     static constexpr size_t kIdsBytes = (size_t)S * kIdsStride * sizeof(int);
     static constexpr size_t kBytes = kIdsBytes + (size_t)S * ROWS * 32 * V * sizeof(double);
 };
@@ -297,13 +298,13 @@ __device__ __forceinline__ void load_prior(const NodeLaunch &a, int node, int ch
     }
 }
 
-template <int D, int V, bool IS_VAR, bool FLAG>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
-__global__ void __launch_bounds__(kThreads, V == 2 ? 2 : 3) k_node_ring(NodeLaunch a, int64_t ntasks) {
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
+__global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int64_t ntasks) {
     constexpr int ROWS = ring_rows<D, IS_VAR>();
     constexpr bool PREG = IS_VAR && !prior_in_ring<D, IS_VAR>();  // prior via registers
     constexpr int ROW = 32 * V;
     constexpr bool FP = !IS_VAR && FLAG;
-    using R = Ring<ROWS, V>;
+    using R = Ring<ROWS, V, MINB>;
     constexpr int S = R::S;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -400,11 +401,11 @@ int ring_v(bool var_side, int deg) {
     return var_side && deg >= 3 ? 1 : 2;
 }
 
-template <int D, int V, bool IS_VAR, bool FLAG>
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB>
 int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
     constexpr int ROWS = ring_rows<D, IS_VAR>();
-    const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS, V>::kBytes;
-    auto kern = k_node_ring<D, V, IS_VAR, FLAG>;
+    const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS, V, MINB>::kBytes;
+    auto kern = k_node_ring<D, V, IS_VAR, FLAG, MINB>;
     static int per_sm = -1, sms = 0;
     static std::mutex mu;
     {
@@ -432,9 +433,25 @@ int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
     return LDPC_OK;
 }
 
+// Resident blocks per SM (sets the ring depth): 2 for V=2, 3 for V=1 by default;
+// LDPC_RING_MINB=3 (V=2) / 4 (V=1) trades ring depth for warps on the variable side.
+int ring_minb(bool var_side, int V) {
+    static const int forced = [] {
+        const char *e = getenv("LDPC_RING_MINB");
+        return e ? atoi(e) : 0;
+    }();
+    if (var_side && forced == (V == 2 ? 3 : 4)) return forced;
+    return V == 2 ? 2 : 3;
+}
+
 template <int D, bool IS_VAR, bool FLAG>
 int launch_ring(const NodeLaunch &a, cudaStream_t st) {
-    return (a.Bp % 64 || ring_v(IS_VAR, D) == 1) ? launch_ring_v<D, 1, IS_VAR, FLAG>(a, st) : launch_ring_v<D, 2, IS_VAR, FLAG>(a, st);
+    if (a.Bp % 64 || ring_v(IS_VAR, D) == 1) {
+        if (IS_VAR && ring_minb(IS_VAR, 1) == 4) return launch_ring_v<D, 1, IS_VAR, FLAG, 4>(a, st);
+        return launch_ring_v<D, 1, IS_VAR, FLAG, 3>(a, st);
+    }
+    if (IS_VAR && ring_minb(IS_VAR, 2) == 3) return launch_ring_v<D, 2, IS_VAR, FLAG, 3>(a, st);
+    return launch_ring_v<D, 2, IS_VAR, FLAG, 2>(a, st);
 }
 
 }  // namespace

@@ -285,6 +285,21 @@ class BatchResult:
 
 # ---- the decoder ----------------------------------------------------------------
 
+class PendingDecode:
+    """One in-flight ParallelDecoder.decode_priors_async batch; keeps its host buffers alive."""
+
+    def __init__(self, decoder, ticket: int, P, result: BatchResult):
+        self._decoder, self._ticket, self._P, self._result = decoder, ticket, P, result
+        self._done = False
+
+    def wait(self) -> BatchResult:
+        if not self._done:
+            self._decoder._wait(self._ticket)
+            self._done = True
+            self._P = None
+        return self._result
+
+
 class ParallelDecoder:
     """GPU drop-in for edgeldpc.engine.ParallelDecoder (engine.py:220-420).
 
@@ -365,6 +380,58 @@ class ParallelDecoder:
                     self._closed = True   # engine.py:389-392: poisoned after a device fault
                 _native.check(rc, "decode")
         return res
+
+    def decode_priors_async(self, P, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
+                            out: BatchResult | None = None, precision: str = "fp64") -> "PendingDecode":
+        """Streaming variant of decode_priors (no reference counterpart): enqueue the H2D copy,
+        the decode and the D2H copy of one batch (B <= max_batch) and return at once; call
+        ``.wait()`` on the result for the BatchResult.  Two batches can be in flight, so the
+        copy of batch k+1 overlaps the decode of batch k.  Results equal decode_priors'.
+        ``P`` and ``out`` should be pinned (torch ``pin_memory()``) for asynchronous copies."""
+        if self._closed:
+            raise RuntimeError("decoder is closed")
+        if max_iterations < 0:
+            raise ValueError("max_iterations must be non-negative")
+        P = np.ascontiguousarray(P, dtype=np.float64)
+        if P.ndim != 2 or P.shape[1] != self.tables.n:
+            raise ValueError(f"expected priors of shape [B, {self.tables.n}]")
+        B = P.shape[0]
+        if not 1 <= B <= self.max_batch:
+            raise ValueError(f"batch {B} outside 1..{self.max_batch}")
+        n, m = self.tables.n, self.tables.m
+        res = out if out is not None else BatchResult(np.empty((B, (n + 31) // 32), np.uint32),
+                                                      np.empty(B, np.uint8), np.empty(B, np.int32),
+                                                      np.empty((B, (m + 31) // 32), np.uint32), n, m)
+        ticket = ctypes.c_int64(-1)
+        with self._lock:
+            rc = _native.lib().ldpc_decoder_submit(
+                self._h, P.ctypes.data, B, int(max_iterations), _flags(early_stop, precision),
+                res.est_bits.ctypes.data, res.success.ctypes.data, res.iterations.ctypes.data,
+                res.syn_bits.ctypes.data, ctypes.byref(ticket))
+            if rc == _native.LDPC_ECUDA or rc == _native.LDPC_ECLOSED:
+                self._closed = True
+            _native.check(rc, "decode")
+        return PendingDecode(self, ticket.value, P, res)
+
+    def decode_stream(self, batches, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
+                      precision: str = "fp64"):
+        """Yield a BatchResult per host priors batch of ``batches``, keeping two batches in flight."""
+        pending = []
+        for P in batches:
+            pending.append(self.decode_priors_async(P, max_iterations, early_stop, precision=precision))
+            if len(pending) == 2:
+                yield pending.pop(0).wait()
+        while pending:
+            yield pending.pop(0).wait()
+
+    def _wait(self, ticket: int) -> None:
+        with self._lock:
+            if self._h is None:
+                raise RuntimeError("decoder is closed")
+            rc = _native.lib().ldpc_decoder_wait(self._h, int(ticket))
+            if rc == _native.LDPC_ECUDA or rc == _native.LDPC_ECLOSED:
+                self._closed = True
+            _native.check(rc, "decode")
 
     def decode_device(self, P_dev, max_iterations: int, early_stop: bool = True, workspace=None,
                       outputs=None, profile: "_native.Profile | None" = None, syndrome_out: bool = True,

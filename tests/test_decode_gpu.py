@@ -236,3 +236,32 @@ def test_graph_replay_reads_fresh_inputs(cuda):
             assert np.array_equal(unpack_bits(est.cpu().numpy().view(np.uint32), H.n), e), call
             assert np.array_equal(its.cpu().numpy(), i), call
             assert np.array_equal(ok.cpu().numpy().astype(bool), s), call
+
+
+def test_streaming_submit_wait_matches_sync(cuda):
+    # decode_priors_async / decode_stream (two batches in flight) give decode_priors' results,
+    # and those equal the oracle's, for batches of varying size and both stop modes
+    import torch
+
+    from oracle import OracleTables
+
+    H = configs.code("C2")
+    O = OracleTables.from_matrix(H)
+    batches = [_frames("C2", B, 1.8, seed=40 + i)[1] for i, B in enumerate((40, 64, 17, 96, 1))]
+    pinned = [torch.from_numpy(P).pin_memory().numpy() for P in batches]
+    with ParallelDecoder(CodeTables.from_matrix(H), max_batch=96) as dec:
+        for early in (True, False):
+            sync = [dec.decode_priors(P, 20, early_stop=early) for P in batches]
+            streamed = list(dec.decode_stream(pinned, 20, early_stop=early))
+            pend = [dec.decode_priors_async(P, 20, early_stop=early) for P in batches[:2]]
+            waited = [p.wait() for p in reversed(pend)][::-1]
+            for i, (a, b) in enumerate(zip(sync, streamed)):
+                assert np.array_equal(a.est_bits, b.est_bits) and np.array_equal(a.syn_bits, b.syn_bits), i
+                assert np.array_equal(a.success, b.success) and np.array_equal(a.iterations, b.iterations), i
+            for a, b in zip(sync, waited):
+                assert np.array_equal(a.est_bits, b.est_bits) and np.array_equal(a.iterations, b.iterations)
+            est, ok, its, z = O.decode_batch(batches[0], 20, fixed_iterations=not early)
+            assert np.array_equal(streamed[0].estimates(), est) and np.array_equal(streamed[0].iterations, its)
+            assert np.array_equal(streamed[0].syndromes(), z) and np.array_equal(streamed[0].success.astype(bool), ok)
+        with pytest.raises(ValueError):
+            dec.decode_priors_async(np.zeros((97, H.n)), 20)

@@ -4,7 +4,7 @@ run() {
 import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$1'.ljust(28), 'ms', round(d['ms_per_step'],3), 'Gbit/s', round(d['value'],3), {k: round(v,3) for k,v in r['kernel_ms_per_step'].items()})"
 }
 run X=0
-run LDPC_RING_V=1
-run LDPC_KERNEL=pipe
+run LDPC_RING_MINB=3
+run LDPC_RING_MINB=4
 run LDPC_KERNEL=reg
 run X=0
