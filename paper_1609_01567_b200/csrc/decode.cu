@@ -50,9 +50,25 @@ bool use_ring(bool var_side, int deg) {
     return var_side && deg >= 2;
 }
 
+size_t chain_scratch_doubles(const ldpc_graph *g, int32_t Bp) {
+    // per phase: every wide node of the side x its tile x the side's max degree (x2 for r and 1-r)
+    size_t wide_c = 0, wide_v = 0;
+    for (const Bucket &b : g->chk_buckets)
+        if (b.deg > kMaxRegDegree) wide_c += (size_t)b.node_count;
+    for (const Bucket &b : g->var_buckets)
+        if (b.deg > kMaxRegDegree) wide_v += (size_t)b.node_count;
+    size_t need = 0;
+    if ((size_t)g->max_dc * kChainTW * sizeof(double) > kChainSmemBudget)
+        need = std::max(need, wide_c * (size_t)g->max_dc * (size_t)Bp);
+    if ((size_t)2 * g->max_dv * kChainTW * sizeof(double) > kChainSmemBudget)
+        need = std::max(need, wide_v * (size_t)g->max_dv * 2 * (size_t)Bp);
+    return need;
+}
+
 size_t workspace_bytes(const ldpc_graph *g, int32_t B) {
     const size_t Bp = (size_t)padded_batch(B), NW = Bp / 32;
     size_t b = 0;
+    b += align256(sizeof(double) * chain_scratch_doubles(g, (int32_t)Bp));
     b += align256(sizeof(double) * (size_t)g->E * Bp);
     b += align256(sizeof(double) * (size_t)g->n * Bp);
     b += align256(sizeof(uint32_t) * (size_t)g->n * NW);
@@ -79,6 +95,8 @@ int carve_workspace(const ldpc_graph *g, int32_t B, void *ws, size_t bytes, Work
         p += align256(sz);
         return r;
     };
+    const size_t scratch = chain_scratch_doubles(g, w->Bp);
+    w->scratch = scratch ? (double *)take(sizeof(double) * scratch) : nullptr;
     w->msg = (double *)take(sizeof(double) * (size_t)g->E * w->Bp);
     w->P = (double *)take(sizeof(double) * (size_t)g->n * w->Bp);
     w->chat = (uint32_t *)take(sizeof(uint32_t) * (size_t)g->n * w->NW);
@@ -171,12 +189,12 @@ struct Prof {
 
 NodeLaunch check_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
     return NodeLaunch{g->chk_off, g->chk_var, g->chk_order, 0, 0, w.msg, w.P, nullptr, done, w.Bp, w.NWs,
-                      (int32_t)g->E, g->n, g->chk_slot, g->chk_slot_ord, g->chk_var_ord, 0};
+                      (int32_t)g->E, g->n, g->chk_slot, g->chk_slot_ord, g->chk_var_ord, 0, w.scratch};
 }
 
 NodeLaunch var_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
     return NodeLaunch{g->var_off, nullptr, g->var_order, 0, 0, w.msg, w.P, w.chat, done, w.Bp, w.NWs,
-                      (int32_t)g->E, g->n, g->var_slot, g->var_slot_ord, nullptr, 0};
+                      (int32_t)g->E, g->n, g->var_slot, g->var_slot_ord, nullptr, 0, w.scratch};
 }
 
 // fp32 fast mode (LDPC_FLAG_FP32): fp32 messages and priors live in the fp64 message buffer

@@ -118,50 +118,115 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
     }
 }
 
-// ---- wide path: one block per (node, tile of TW codewords) -----------------
-// Shared memory holds b_i and the prefix products for the tile; worker w of
-// the block produces outputs k = w, w + NWK, ... (NWK = 256 / TW workers).
-template <bool FROM_PRIOR>
-__global__ void __launch_bounds__(kThreads) k_check_wide(NodeLaunch a, int TW, int max_deg) {
-    extern __shared__ double sm[];
-    double *b = sm;                         // [max_deg][TW]
-    double *pre = sm + (size_t)max_deg * TW; // [max_deg][TW]
+// ---- high-degree path: chains of outputs over shared-memory b ------------------
+// One block per (check, tile of TW codewords), 1024 threads; any degree.  The d outputs need
+// d(d-1)/2 ordered multiplies per codeword (exactness forbids a suffix-product
+// shortcut), so the work is fp64-bound for d >> 16 and is spread as:
+//   * b_i = 1 - 2 q_i of the tile staged in shared memory ([d][TW]), or in the
+//     workspace scratch when d is past the shared-memory budget; after that barrier
+//     the in-place slot writes cannot race a read;
+//   * outputs in groups of R = 8; lane = (codeword c = lane % TW, part h = lane / TW)
+//     and each thread carries CPT = R*TW/32 output chains of its group, so one
+//     shared load feeds CPT independent multiplies, and the TW lanes reading a row
+//     form a conflict-free wavefront (the 32/TW parts read the same row: broadcast);
+//   * warp w takes groups w, 63-w, 64+w, 127-w, ... : ascending (so one running
+//     prefix 1*b_0*...*b_{k-1} carried across its groups replaces a sequential
+//     prefix pass), and balanced (each band of 64 pairs a long suffix with a short
+//     one).  The carry rides in the body loop as one more chain.
+constexpr int kWideR = 8;
+constexpr int kWideThreads = 1024;
+
+__device__ __forceinline__ int chains_group(int w, int t) {  // t-th group of warp w (32 warps)
+    const int band = t >> 1;
+    return band * 64 + ((t & 1) ? 63 - w : w);
+}
+
+template <int TW, bool FROM_PRIOR, bool GS>  // GS: staging in global scratch (degrees past the smem budget)
+__global__ void __launch_bounds__(kWideThreads) k_check_chains(NodeLaunch a, int max_deg) {
+    constexpr int CPT = kWideR * TW / 32;   // chains per thread
+    static_assert(CPT >= 1 && kWideThreads == 1024, "TW must be >= 4; 32 warps");
+    extern __shared__ double smem_b[];
+    double *b = GS ? a.scratch + (size_t)blockIdx.x * max_deg * TW : smem_b;  // [d][TW]
     const int tile = blockIdx.x / a.node_count;  // tile-major: all nodes of tile 0 first
     const int ni = blockIdx.x - tile * a.node_count;
-    const int c = threadIdx.x % TW;
-    const int worker = threadIdx.x / TW;
-    const int nwk = blockDim.x / TW;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = lane % TW, h = lane / TW;
     const int cw = tile * TW + c;
     if (a.done != nullptr) {
         const int w0 = (tile * TW) >> 5;
         const uint32_t mask = (TW >= 32) ? 0xffffffffu : (((1u << TW) - 1u) << ((tile * TW) & 31));
-        bool all = true;
-        for (int w = w0; w < w0 + (TW + 31) / 32; w++) all = all && ((a.done[w] & mask) == mask);
-        if (all) return;
+        if ((a.done[w0] & mask) == mask) return;
     }
     const int node = __ldg(a.order + a.node_begin + ni);
     const int pos0 = __ldg(a.off + node);
     const int d = __ldg(a.off + node + 1) - pos0;
-    for (int i = worker; i < d; i += nwk) {
-        double q = FROM_PRIOR ? __ldg(a.P + cofs(a.p_rows, __ldg(a.idx + pos0 + i), cw))
-                              : ld_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + i) : pos0 + i, cw));
-        b[i * TW + c] = __dsub_rn(1.0, __dmul_rn(2.0, q));
+    const int G = (d + kWideR - 1) / kWideR;
+    for (int e = threadIdx.x; e < d * TW; e += blockDim.x) {
+        const int i = e / TW, cc = e - i * TW;
+        const int cwe = tile * TW + cc;
+        const double q = FROM_PRIOR ? __ldg(a.P + cofs(a.p_rows, __ldg(a.idx + pos0 + i), cwe))
+                                    : ld_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + i) : pos0 + i, cwe));
+        b[e] = __dsub_rn(1.0, __dmul_rn(2.0, q));
     }
     __syncthreads();
-    if (worker == 0) {
-        double p = 1.0;
-        for (int i = 0; i < d; i++) {
-            pre[i * TW + c] = p;
-            p = __dmul_rn(p, b[i * TW + c]);
+    const double *bc = b + c;
+    auto B = [&](int i) { return bc[i * TW]; };
+    const int j0 = h * CPT;  // this thread's outputs in a group: k0 + j0 .. k0 + j0 + CPT - 1
+    // running prefix: pre = 1*b_0*...*b_{at-1}, left to right from 1.0 (serial.py:105-110 order)
+    double pre = 1.0;
+    int at = 0;
+    for (int t = 0;; t++) {
+        const int g = chains_group(warp, t);
+        if (g >= G) break;
+        const int k0 = g * kWideR, kb = k0 + j0;       // first output of this thread
+        const int gn = chains_group(warp, t + 1);
+        const int next = gn * kWideR + j0;             // where the carry must stop (next group's kb)
+        for (; at < kb; at++) pre = __dmul_rn(pre, at < d ? B(at) : 1.0);
+        double acc[CPT];
+        double p = pre;
+#pragma unroll
+        for (int j = 0; j < CPT; j++) {
+            acc[j] = p;
+            if (j + 1 < CPT) p = __dmul_rn(p, kb + j < d ? B(kb + j) : 1.0);
         }
-    }
-    __syncthreads();
-    // fold outputs so each worker gets a mix of long and short suffix chains
-    for (int j = worker; j < d; j += nwk) {
-        const int k = (j & 1) ? (d - 1 - (j >> 1)) : (j >> 1);
-        double acc = pre[k * TW + c];
-        for (int i = k + 1; i < d; i++) acc = __dmul_rn(acc, b[i * TW + c]);
-        st_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + k) : pos0 + k, cw), __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc))));
+        // head: position kb + j multiplies the chains whose output is below it
+#pragma unroll
+        for (int j = 1; j < CPT; j++) {
+            if (kb + j < d) {
+                const double x = B(kb + j);
+#pragma unroll
+                for (int jj = 0; jj < j; jj++) acc[jj] = __dmul_rn(acc[jj], x);
+            }
+        }
+        // body with the carry: positions kb .. next-1 also extend the running prefix
+        for (; at < kb + CPT && at < next; at++) pre = __dmul_rn(pre, at < d ? B(at) : 1.0);
+        int i = kb + CPT;
+        const int stop_carry = min(next, d);
+        for (; i < stop_carry; i++) {
+            const double x = B(i);
+#pragma unroll
+            for (int j = 0; j < CPT; j++) acc[j] = __dmul_rn(acc[j], x);
+            pre = __dmul_rn(pre, x);
+        }
+        if (i > at) at = i;
+        for (; i + 1 < d; i += 2) {
+            const double x0 = B(i), x1 = B(i + 1);
+#pragma unroll
+            for (int j = 0; j < CPT; j++) acc[j] = __dmul_rn(__dmul_rn(acc[j], x0), x1);
+        }
+        if (i < d) {
+            const double x = B(i);
+#pragma unroll
+            for (int j = 0; j < CPT; j++) acc[j] = __dmul_rn(acc[j], x);
+        }
+        // r_k = 1 - (0.5 + 0.5 * prod_k)
+#pragma unroll
+        for (int j = 0; j < CPT; j++) {
+            const int k = kb + j;
+            if (k < d)
+                st_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + k) : pos0 + k, cw),
+                       __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc[j]))));
+        }
     }
 }
 
@@ -207,22 +272,30 @@ int launch_check_bucket(const NodeLaunch &a, int deg, bool from_prior, cudaStrea
     }
 }
 
-int launch_check_wide(const NodeLaunch &a, int max_deg, bool from_prior, cudaStream_t s) {
-    if (a.node_count == 0) return LDPC_OK;
-    const size_t budget = 200 * 1024;
-    int TW = 32;
-    while (TW > 1 && (size_t)2 * max_deg * TW * sizeof(double) > budget) TW >>= 1;
-    const size_t smem = (size_t)2 * max_deg * TW * sizeof(double);
-    if (smem > budget) {
-        set_error("check degree %d exceeds the shared-memory staging limit", max_deg);
-        return LDPC_EINVAL;
-    }
-    auto kern = from_prior ? k_check_wide<true> : k_check_wide<false>;
-    LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int TW, bool GS>
+int launch_chains(const NodeLaunch &a, int max_deg, size_t smem, bool from_prior, cudaStream_t s) {
+    auto kern = from_prior ? k_check_chains<TW, true, GS> : k_check_chains<TW, false, GS>;
+    if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (int64_t)a.node_count * (a.Bp / TW);
-    kern<<<(unsigned)blocks, kThreads, smem, s>>>(a, TW, max_deg);
+    kern<<<(unsigned)blocks, kWideThreads, smem, s>>>(a, max_deg);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
+}
+
+int launch_check_wide(const NodeLaunch &a, int max_deg, bool from_prior, cudaStream_t s) {
+    if (a.node_count == 0) return LDPC_OK;
+    // the widest tile (more chains per thread) whose b fits in shared memory; past that,
+    // 16-codeword tiles staged in the workspace scratch.  LDPC_WIDE_TW=4|8|16 forces a tile.
+    static const int forced = [] {
+        const char *e = getenv("LDPC_WIDE_TW");
+        return e ? atoi(e) : 0;
+    }();
+    auto smem = [&](int tw) { return (size_t)max_deg * tw * sizeof(double); };
+    if ((forced == 0 || forced == 16) && smem(16) <= kChainSmemBudget) return launch_chains<16, false>(a, max_deg, smem(16), from_prior, s);
+    if ((forced == 0 || forced == 8) && smem(8) <= kChainSmemBudget) return launch_chains<8, false>(a, max_deg, smem(8), from_prior, s);
+    if ((forced == 0 || forced == 4) && smem(4) <= kChainSmemBudget) return launch_chains<4, false>(a, max_deg, smem(4), from_prior, s);
+    LDPC_ARG_CHECK(a.scratch != nullptr, "check degree %d needs the workspace scratch (workspace too old?)", max_deg);
+    return launch_chains<kChainTW, true>(a, max_deg, 0, from_prior, s);
 }
 
 }  // namespace ldpc

@@ -169,19 +169,32 @@ __global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_re
     }
 }
 
-// ---- wide path: one block per (variable, tile of TW codewords) -------------
-template <bool WRITE_Q>
-__global__ void __launch_bounds__(kThreads) k_var_wide(NodeLaunch a, int TW, int max_deg) {
-    extern __shared__ double sm[];
-    double *r = sm;                                  // [max_deg][TW]
-    double *pre0 = r + (size_t)max_deg * TW;         // [max_deg+1][TW]
-    double *pre1 = pre0 + (size_t)(max_deg + 1) * TW; // [max_deg+1][TW]
-    int *spos = reinterpret_cast<int *>(pre1 + (size_t)(max_deg + 1) * TW);  // [max_deg]
-    const int tile = blockIdx.x / a.node_count;  // tile-major: all nodes of tile 0 first
+// ---- high-degree path: chains of outputs over shared-memory r / 1-r -----------
+// Same structure as k_check_chains (kernels_check.cu): one block of 1024 threads per
+// (variable, tile of TW codewords), any degree; r and 1 - r staged in shared memory
+// (or the workspace scratch past the shared-memory budget); outputs in
+// groups of R = 8 with CPT = R*TW/32 chains per thread, each chain the pair
+// (q0, q1) of serial.py:77-88; warps take groups w, 63-w, 64+w, ... ascending so a
+// running prefix pair ((1-p)*prod(1-r_i), p*prod(r_i)) is carried across groups.
+// Warp 0 part 0 carries its prefix to the end: the estimate's (Q0, Q1).
+constexpr int kChainR = 8;
+constexpr int kChainThreads = 1024;
+
+__device__ __forceinline__ int var_chains_group(int w, int t) {
+    const int band = t >> 1;
+    return band * 64 + ((t & 1) ? 63 - w : w);
+}
+
+template <int TW, bool WRITE_Q, bool GS>  // GS: staging in global scratch (degrees past the smem budget)
+__global__ void __launch_bounds__(kChainThreads) k_var_chains(NodeLaunch a, int max_deg) {
+    constexpr int CPT = kChainR * TW / 32;
+    static_assert(CPT >= 1, "TW must be >= 4");
+    extern __shared__ double smem_rs[];
+    double *sm = GS ? a.scratch + (size_t)blockIdx.x * max_deg * TW * 2 : smem_rs;
+    const int tile = blockIdx.x / a.node_count;
     const int ni = blockIdx.x - tile * a.node_count;
-    const int c = threadIdx.x % TW;
-    const int worker = threadIdx.x / TW;
-    const int nwk = blockDim.x / TW;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = lane % TW, h = lane / TW;
     const int cw = tile * TW + c;
     const int w = (tile * TW) >> 5;
     const uint32_t tmask = (TW >= 32) ? 0xffffffffu : (((1u << TW) - 1u) << ((tile * TW) & 31));
@@ -189,63 +202,120 @@ __global__ void __launch_bounds__(kThreads) k_var_wide(NodeLaunch a, int TW, int
     const int node = __ldg(a.order + a.node_begin + ni);
     const int e0 = __ldg(a.off + node);
     const int d = __ldg(a.off + node + 1) - e0;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) spos[i] = a.slot ? __ldg(a.slot + e0 + i) : e0 + i;
-    __syncthreads();
-    for (int i = worker; i < d; i += nwk) r[i * TW + c] = ld_msg(a.msg + cofs(a.msg_rows, spos[i], cw));
-    __syncthreads();
-    if (worker == 0) {
-        const double p = __ldg(a.P + cofs(a.p_rows, node, cw));
-        double x0 = __dsub_rn(1.0, p), x1 = p;
-        for (int i = 0; i < d; i++) {
-            pre0[i * TW + c] = x0;
-            pre1[i * TW + c] = x1;
-            const double ri = r[i * TW + c];
-            x0 = __dmul_rn(x0, __dsub_rn(1.0, ri));
-            x1 = __dmul_rn(x1, ri);
-        }
-        pre0[d * TW + c] = x0;
-        pre1[d * TW + c] = x1;
+    const int G = (d + kChainR - 1) / kChainR;
+    double *rs = sm;                    // [d][TW] r_i
+    double *os = sm + (size_t)d * TW;   // [d][TW] 1 - r_i
+    for (int e = threadIdx.x; e < d * TW; e += blockDim.x) {
+        const int i = e / TW, cc = e - i * TW;
+        const double r = ld_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + e0 + i) : e0 + i, tile * TW + cc));
+        rs[e] = r;
+        os[e] = __dsub_rn(1.0, r);
     }
+    const double pj = __ldg(a.P + cofs(a.p_rows, node, cw));
     __syncthreads();
-    if (WRITE_Q) {
-        for (int j = worker; j < d; j += nwk) {
-            const int k = (j & 1) ? (d - 1 - (j >> 1)) : (j >> 1);
-            double q0 = pre0[k * TW + c], q1 = pre1[k * TW + c];
-            for (int i = k + 1; i < d; i++) {
-                const double ri = r[i * TW + c];
-                q0 = __dmul_rn(q0, __dsub_rn(1.0, ri));
-                q1 = __dmul_rn(q1, ri);
+    const double *rc = rs + c, *oc = os + c;
+    double pre0 = __dsub_rn(1.0, pj), pre1 = pj;  // running prefix pair over positions < at
+    int at = 0;
+    auto step = [&](int i) {
+        if (i < d) {
+            pre0 = __dmul_rn(pre0, oc[i * TW]);
+            pre1 = __dmul_rn(pre1, rc[i * TW]);
+        }
+    };
+    if constexpr (WRITE_Q) {
+        const int j0 = h * CPT;
+        for (int t = 0;; t++) {
+            const int g = var_chains_group(warp, t);
+            if (g >= G) break;
+            const int kb = g * kChainR + j0;
+            const int next = var_chains_group(warp, t + 1) * kChainR + j0;
+            for (; at < kb; at++) step(at);
+            double a0[CPT], a1[CPT];
+            double p0 = pre0, p1 = pre1;
+#pragma unroll
+            for (int j = 0; j < CPT; j++) {
+                a0[j] = p0;
+                a1[j] = p1;
+                if (j + 1 < CPT && kb + j < d) {
+                    p0 = __dmul_rn(p0, oc[(kb + j) * TW]);
+                    p1 = __dmul_rn(p1, rc[(kb + j) * TW]);
+                }
             }
-            const double den = __dadd_rn(q0, q1);
-            bool ok;
-            double q = ddiv_fast(q1, den, ok);
-            if (!ok) q = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
-            st_msg(a.msg + cofs(a.msg_rows, spos[k], cw), q);
+#pragma unroll
+            for (int j = 1; j < CPT; j++) {
+                if (kb + j < d) {
+                    const double x0 = oc[(kb + j) * TW], x1 = rc[(kb + j) * TW];
+#pragma unroll
+                    for (int jj = 0; jj < j; jj++) {
+                        a0[jj] = __dmul_rn(a0[jj], x0);
+                        a1[jj] = __dmul_rn(a1[jj], x1);
+                    }
+                }
+            }
+            for (; at < kb + CPT && at < next; at++) step(at);
+            int i = kb + CPT;
+            const int stop_carry = min(next, d);
+            for (; i < stop_carry; i++) {
+                const double x0 = oc[i * TW], x1 = rc[i * TW];
+#pragma unroll
+                for (int j = 0; j < CPT; j++) {
+                    a0[j] = __dmul_rn(a0[j], x0);
+                    a1[j] = __dmul_rn(a1[j], x1);
+                }
+                pre0 = __dmul_rn(pre0, x0);
+                pre1 = __dmul_rn(pre1, x1);
+            }
+            if (i > at) at = i;
+            for (; i < d; i++) {
+                const double x0 = oc[i * TW], x1 = rc[i * TW];
+#pragma unroll
+                for (int j = 0; j < CPT; j++) {
+                    a0[j] = __dmul_rn(a0[j], x0);
+                    a1[j] = __dmul_rn(a1[j], x1);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < CPT; j++) {
+                const int k = kb + j;
+                if (k < d) {
+                    const double den = __dadd_rn(a0[j], a1[j]);
+                    bool ok;
+                    double q = ddiv_fast(a1[j], den, ok);
+                    if (!ok) q = (den == 0.0) ? 0.5 : __ddiv_rn(a1[j], den);
+                    st_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + e0 + k) : e0 + k, cw), q);
+                }
+            }
         }
     }
-    if (worker == 0) {
-        // bits of this tile's codewords; tiles smaller than a word share it -> atomics
-        const bool one = !(pre0[d * TW + c] > pre1[d * TW + c]);
+    // estimate (serial.py:125-132): warp 0, part 0 holds or completes the full products
+    if (warp == 0) {
+        if (h == 0)
+            for (; at < d; at++) step(at);
+        const bool one = !(pre0 > pre1);
         const uint32_t keep = a.done ? a.done[w] : 0u;
-        uint32_t bits = 0;
-        if (TW >= 32) {
-            bits = __ballot_sync(0xffffffffu, one);
-            if (c == 0) {
-                uint32_t *dst = a.chat + (size_t)node * a.NW + w;
-                *dst = keep ? ((bits & ~keep) | (*dst & keep)) : bits;
-            }
-        } else {
-            // TW < 32: the worker-0 threads are lanes 0..TW-1 of warp 0
-            const uint32_t sub = __ballot_sync((TW == 32) ? 0xffffffffu : ((1u << TW) - 1u), one);
-            if (c == 0) {
+        const uint32_t sub = __ballot_sync(0xffffffffu, h == 0 && one);  // bit c of lanes 0..TW-1
+        if (lane == 0) {
+            uint32_t *dst = a.chat + (size_t)node * a.NW + w;
+            if (TW >= 32) {
+                *dst = keep ? ((sub & ~keep) | (*dst & keep)) : sub;
+            } else {  // tiles smaller than a word share it -> atomics
                 const int sh = (tile * TW) & 31;
                 const uint32_t upd = tmask & ~keep;
-                uint32_t *dst = a.chat + (size_t)node * a.NW + w;
                 atomicAnd(dst, ~upd);
                 atomicOr(dst, (sub << sh) & upd);
             }
         }
     }
+}
+
+template <int TW, bool GS>
+int launch_var_chains(const NodeLaunch &a, int max_deg, size_t smem, bool write_q, cudaStream_t s) {
+    auto kern = write_q ? k_var_chains<TW, true, GS> : k_var_chains<TW, false, GS>;
+    if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t blocks = (int64_t)a.node_count * (a.Bp / TW);
+    kern<<<(unsigned)blocks, kChainThreads, smem, s>>>(a, max_deg);
+    LDPC_CHECK_LAUNCH();
+    return LDPC_OK;
 }
 
 int vpolicy_var(int deg) {
@@ -291,23 +361,18 @@ int launch_var_bucket(const NodeLaunch &a, int deg, bool write_q, cudaStream_t s
 
 int launch_var_wide(const NodeLaunch &a, int max_deg, bool write_q, cudaStream_t s) {
     if (a.node_count == 0) return LDPC_OK;
-    const size_t budget = 200 * 1024;
-    auto bytes = [&](int TW) {
-        return ((size_t)max_deg + 2 * ((size_t)max_deg + 1)) * TW * sizeof(double) + (size_t)max_deg * sizeof(int);
-    };
-    int TW = 32;
-    while (TW > 1 && bytes(TW) > budget) TW >>= 1;
-    if (bytes(TW) > budget) {
-        set_error("variable degree %d exceeds the shared-memory staging limit", max_deg);
-        return LDPC_EINVAL;
-    }
-    const size_t smem = bytes(TW);
-    auto kern = write_q ? k_var_wide<true> : k_var_wide<false>;
-    LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t blocks = (int64_t)a.node_count * (a.Bp / TW);
-    kern<<<(unsigned)blocks, kThreads, smem, s>>>(a, TW, max_deg);
-    LDPC_CHECK_LAUNCH();
-    return LDPC_OK;
+    // the widest tile whose r and 1-r fit in shared memory; past that, 16-codeword tiles
+    // staged in the workspace scratch.  LDPC_WIDE_TW=4|8|16 forces a tile.
+    static const int forced = [] {
+        const char *e = getenv("LDPC_WIDE_TW");
+        return e ? atoi(e) : 0;
+    }();
+    auto smem = [&](int tw) { return (size_t)2 * max_deg * tw * sizeof(double); };
+    if ((forced == 0 || forced == 16) && smem(16) <= kChainSmemBudget) return launch_var_chains<16, false>(a, max_deg, smem(16), write_q, s);
+    if ((forced == 0 || forced == 8) && smem(8) <= kChainSmemBudget) return launch_var_chains<8, false>(a, max_deg, smem(8), write_q, s);
+    if ((forced == 0 || forced == 4) && smem(4) <= kChainSmemBudget) return launch_var_chains<4, false>(a, max_deg, smem(4), write_q, s);
+    LDPC_ARG_CHECK(a.scratch != nullptr, "variable degree %d needs the workspace scratch", max_deg);
+    return launch_var_chains<kChainTW, true>(a, max_deg, 0, write_q, s);
 }
 
 }  // namespace ldpc

@@ -175,3 +175,32 @@ def test_fast_division_is_bitwise_ddiv_rn(cuda):
         _native.check(rc, "selftest")
         assert res[0] == 0, f"{res[0]} mismatches"
         assert res[1] > (1 << 26)
+
+
+def test_unbounded_degree_phases_and_decode(cuda):
+    # "no bound on node degree": a check of degree 13000 (past the shared-memory staging of
+    # every tile width, so the chains kernel stages in the workspace scratch) and a variable
+    # of degree 4000 (same for r / 1-r), bit-exact against the oracle in both phases and a decode
+    from oracle import OracleTables
+    from paper_1609_01567_b200 import ParallelDecoder, generate_irregular_code, priors_awgn_batch
+
+    H = generate_irregular_code({4000: 1, 2: 15999}, 6000, seed=5, check_degrees={13000: 1})
+    dv, dc = H.degrees()
+    assert dv.max() == 4000 and dc.max() == 13000
+    T = CodeTables.from_matrix(H)
+    O = OracleTables.from_matrix(H)
+    rng = np.random.default_rng(11)
+    B = 2
+    P = rng.uniform(size=(B, H.n))
+    R = rng.uniform(size=(B, H.total_edges))
+    Q = rng.uniform(size=(B, H.total_edges))
+    assert np.array_equal(bits(values_to_variable(Q, T)), bits(np.stack([O.values_to_variable(q) for q in Q])))
+    assert np.array_equal(bits(values_to_check(P, R, T)), bits(np.stack([O.values_to_check(p, r) for p, r in zip(P, R)])))
+    assert np.array_equal(estimate(P, R, T), np.stack([O.estimate(p, r) for p, r in zip(P, R)]))
+    s2 = 0.8
+    Pd = priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((B, H.n)), s2)
+    with ParallelDecoder(T, max_batch=B) as dec:
+        res = dec.decode_priors(Pd, 2, early_stop=False)
+    est, ok, its, z = O.decode_batch(Pd, 2, fixed_iterations=True)
+    assert np.array_equal(res.estimates(), est) and np.array_equal(res.syndromes(), z)
+    assert np.array_equal(res.success.astype(bool), ok) and np.array_equal(res.iterations, its)
