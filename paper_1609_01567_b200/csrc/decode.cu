@@ -572,11 +572,12 @@ extern "C" int ldpc_phase_f32(const ldpc_graph *g, int phase, const double *p_de
 // decode runs ~20% below the full-batch rate).
 namespace {
 constexpr int kMaxChunks = 64;
-constexpr int kLanes = 2;
+constexpr int kLanes = 4;         // compute streams available
+constexpr int kDefaultLanes = 2;  // used by default (LDPC_E2E_LANES=1..4 overrides)
 int e2e_lanes() {
     static const int v = [] {
         const char *e = getenv("LDPC_E2E_LANES");
-        const int x = e ? atoi(e) : kLanes;
+        const int x = e ? atoi(e) : kDefaultLanes;
         return x < 1 ? 1 : (x > kLanes ? kLanes : x);
     }();
     return v;
@@ -615,7 +616,7 @@ struct ldpc_decoder {
 
 static void decoder_free(ldpc_decoder *d) {
     if (!d) return;
-    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_out})
+    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_comp[2], d->s_comp[3], d->s_out})
         if (s) cudaStreamSynchronize(s);
     for (void *w : d->ws) cudaFree(w);
     cudaFree(d->ws_full);
@@ -636,21 +637,34 @@ static void decoder_free(ldpc_decoder *d) {
     for (int i = 0; i < kMaxChunks; i++)
         for (cudaEvent_t e : {d->in_ready[i], d->decoded[i]})
             if (e) cudaEventDestroy(e);
-    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_out})
+    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_comp[2], d->s_comp[3], d->s_out})
         if (s) cudaStreamDestroy(s);
     delete d;
 }
 
-// sub-batch sizes for a batch of B: 64, 96, 144, ... capped at sub, the last one takes the rest
+// Sub-batch sizes for a batch of B: multiples of 64 codewords (the kernels pad a
+// batch to a multiple of 64, so e.g. 96 would cost the work of 128), growing
+// geometrically from 64 (LDPC_E2E_GROWTH, x100, default 150), capped at `sub`; a
+// remainder smaller than the sub-batch before it is merged into that one, since
+// the last decode is exposed after the last copy.
 static std::vector<int32_t> chunk_plan(int32_t B, int32_t sub) {
+    static const int growth = [] {
+        const char *e = getenv("LDPC_E2E_GROWTH");
+        return e ? std::max(101, atoi(e)) : 150;
+    }();
     std::vector<int32_t> v;
-    int32_t b = std::min<int32_t>(sub, 64);
+    const int32_t cap = std::max<int32_t>(64, sub / 64 * 64);
+    int32_t b = std::min<int32_t>(cap, 64);
     for (int32_t c0 = 0; c0 < B;) {
         int32_t take = std::min(b, B - c0);
         if ((int)v.size() == kMaxChunks - 1) take = B - c0;  // keep within the event budget
         v.push_back(take);
         c0 += take;
-        b = std::min<int32_t>(sub, std::max<int32_t>(b, (b * 3 / 2) / 32 * 32));
+        b = std::min<int32_t>(cap, std::max<int32_t>(b + 64, (b * growth / 100) / 64 * 64));
+    }
+    if (v.size() >= 2 && v.back() < v[v.size() - 2]) {
+        v[v.size() - 2] += v.back();
+        v.pop_back();
     }
     return v;
 }
@@ -745,7 +759,7 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
             cuda(cudaMemcpyAsync(syn_bits_host + c0 * RWm, d->syn + c0 * RWm, sizeof(uint32_t) * RWm * b,
                                  cudaMemcpyDeviceToHost, d->s_out), "D2H syndrome");
     }
-    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_out})
+    for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_comp[2], d->s_comp[3], d->s_out})
         if (s) cuda(cudaStreamSynchronize(s), "decode");
     if (rc == LDPC_OK && e != cudaSuccess) rc = LDPC_ECUDA;
     if (rc == LDPC_ECUDA) d->poisoned = true;  // mirrors engine.py:389-392: refuse further use

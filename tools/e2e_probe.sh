@@ -1,8 +1,7 @@
-# e2e (host API) timing vs compute lanes and sub-batch plan
+# e2e (host API) timing vs sub-batch plan growth and compute lanes
 {
-timeout 600 python -m pytest tests/test_decode_gpu.py -q -m gpu -x -p no:cacheprovider 2>&1 | tail -2
-for lanes in 1 2; do for sb in 0 256; do
-LDPC_E2E_LANES=$lanes timeout 300 python bench.py --no-cpu --no-fast --steps 10 --warmup 3 --sub-batch $sb 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('lanes $lanes sub $sb', 'device ms', round(d['ms_per_step'],3), 'e2e ms', round(d['e2e']['ms_per_step'],3), 'e2e Gbit/s', round(d['e2e']['value'],3))"
-done; done
+for v in "X=0" "LDPC_E2E_GROWTH=170" "LDPC_E2E_GROWTH=200" "LDPC_E2E_LANES=1" "LDPC_E2E_LANES=3" "X=1"; do
+env $v timeout 300 python bench.py --no-cpu --no-fast --steps 20 --warmup 3 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$v'.ljust(30), 'device ms', round(d['ms_per_step'],3), 'e2e ms', round(d['e2e']['ms_per_step'],3), 'e2e Gbit/s', round(d['e2e']['value'],3), 'stream ms', round(d['e2e_stream']['ms_per_step'],3))"
+done
 } 2>&1 | tee gpurun_out/e2e_probe.log
