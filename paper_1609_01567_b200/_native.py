@@ -25,6 +25,8 @@ LDPC_ECLOSED = -4
 FLAG_EARLY_STOP = 0
 FLAG_FIXED_ITERS = 1
 FLAG_FP32 = 2
+FLAG_STREAMING = 4
+FLAG_ONCHIP = 8
 
 VARIABLE = 0
 CHECK = 1

@@ -378,15 +378,27 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
     LDPC_ARG_CHECK(g != nullptr, "NULL graph");
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
     LDPC_ARG_CHECK(p_dev && est_bits_dev && success_dev && iters_dev, "NULL output/input pointer");
-    LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32)) == 0, "unknown flags 0x%x", flags);
+    LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32 | LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP)) == 0,
+                   "unknown flags 0x%x", flags);
     const bool fast = (flags & LDPC_FLAG_FP32) != 0;
     LDPC_ARG_CHECK(!fast || (g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree),
                    "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
+    // small codes: the whole decode on chip (onchip.cu), unless the caller forces streaming
+    const bool want_onchip = (flags & LDPC_FLAG_ONCHIP) != 0;
+    const int cs = (fast || (flags & LDPC_FLAG_STREAMING)) ? 0
+                   : want_onchip ? onchip_cluster_size(g, true) : (onchip_auto(g, B) ? 1 : 0);
+    LDPC_ARG_CHECK(!(flags & LDPC_FLAG_ONCHIP) || (cs > 0 && !(flags & LDPC_FLAG_STREAMING)),
+                   "the on-chip schedule needs a code whose messages fit 8 CTAs' shared memory (fp64)");
+    if (cs > 0 && prof_host == nullptr) {
+        LDPC_ARG_CHECK(B >= 1, "batch must be at least 1");
+        return launch_onchip(g, cs, p_dev, B, max_iterations, early, est_bits_dev, success_dev, iters_dev,
+                             syn_bits_dev, s);
+    }
     Workspace w;
     int rc = carve_workspace(g, B, workspace_dev, workspace_bytes_, &w);
     if (rc) return rc;
-    cudaStream_t s = (cudaStream_t)stream;
-    const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
     auto sequence = [&](Prof &prof) -> int {
         const int64_t n = g->n, m = g->m;
         RUN(LDPC_KCLASS_LAYOUT, 16 * n * B, launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s));
@@ -461,15 +473,18 @@ extern "C" int ldpc_decode_channel(const ldpc_graph *g, uint64_t seed, uint64_t 
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
     LDPC_ARG_CHECK(sigma2 > 0.0, "sigma2 must be positive");
     LDPC_ARG_CHECK(est_bits_dev && success_dev && iters_dev, "NULL output pointer");
-    LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32)) == 0, "unknown flags 0x%x", flags);
+    LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32 | LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP)) == 0,
+                   "unknown flags 0x%x", flags);
     const bool fast = (flags & LDPC_FLAG_FP32) != 0;
     LDPC_ARG_CHECK(!fast || (g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree),
                    "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
+    // (device-generated priors land chunk-major, so this path always streams)
+    LDPC_ARG_CHECK(!(flags & LDPC_FLAG_ONCHIP), "decode_channel runs the streaming schedule");
     Workspace w;
     int rc = carve_workspace(g, B, workspace_dev, workspace_bytes_, &w);
     if (rc) return rc;
-    cudaStream_t s = (cudaStream_t)stream;
-    const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
     Prof prof;
     if ((rc = launch_channel_priors(seed, point, frame0, B, g->n, sigma2, w.P, w.Bp, s))) return rc;
     if ((rc = run_decode(g, w, max_iterations, early, s, prof, fast))) return rc;

@@ -157,11 +157,20 @@ def _dev(a: np.ndarray, device: int):
 
 # ---- single phases (serial.py:63-147 signatures, any batch) -------------------
 
-def _flags(early_stop: bool, precision: str) -> int:
+SCHEDULES = ("auto", "stream", "onchip")
+
+
+def _flags(early_stop: bool, precision: str, schedule: str = "auto") -> int:
+    """schedule: "auto" decodes small codes entirely on chip (one CTA or thread-block cluster per
+    codeword, onchip.cu) and streams the rest; "stream" / "onchip" force one (identical results)."""
     if precision not in ("fp64", "fp32"):
         raise ValueError("precision must be 'fp64' (exact) or 'fp32' (fast mode)")
+    if schedule not in SCHEDULES:
+        raise ValueError(f"schedule must be one of {SCHEDULES}")
     return ((_native.FLAG_EARLY_STOP if early_stop else _native.FLAG_FIXED_ITERS)
-            | (_native.FLAG_FP32 if precision == "fp32" else 0))
+            | (_native.FLAG_FP32 if precision == "fp32" else 0)
+            | (_native.FLAG_STREAMING if schedule == "stream" else 0)
+            | (_native.FLAG_ONCHIP if schedule == "onchip" else 0))
 
 
 def values_to_check(p, r, tables: CodeTables, precision: str = "fp64") -> np.ndarray:
@@ -341,17 +350,18 @@ class ParallelDecoder:
         return self.decode_priors(p.reshape(1, -1), max_iterations)[0]
 
     def decode_batch(self, Y, sigma2, max_iterations: int = DEFAULT_MAX_ITERATIONS,
-                     early_stop: bool = True, precision: str = "fp64") -> BatchResult:
+                     early_stop: bool = True, precision: str = "fp64", schedule: str = "auto") -> BatchResult:
         """B received frames [B, n] (sigma2 scalar or [B]) -> BatchResult."""
         if self._closed:
             raise RuntimeError("decoder is closed")
         Y = np.asarray(Y, dtype=np.float64)
         if Y.ndim != 2 or Y.shape[1] != self.tables.n:
             raise ValueError(f"expected frames of {self.tables.n} observations")
-        return self.decode_priors(priors_awgn_batch(Y, sigma2), max_iterations, early_stop, precision=precision)
+        return self.decode_priors(priors_awgn_batch(Y, sigma2), max_iterations, early_stop, precision=precision,
+                                  schedule=schedule)
 
     def decode_priors(self, P, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
-                      out: BatchResult | None = None, precision: str = "fp64") -> BatchResult:
+                      out: BatchResult | None = None, precision: str = "fp64", schedule: str = "auto") -> BatchResult:
         """Host priors [B, n] (pinned memory recommended) -> host BatchResult.
 
         precision="fp32": fast mode, same algorithm in fp32 (not bit-exact; DESIGN.md tolerance)."""
@@ -368,7 +378,7 @@ class ParallelDecoder:
                                                       np.empty(B, np.uint8), np.empty(B, np.int32),
                                                       np.empty((B, (m + 31) // 32), np.uint32), n, m)
         L = _native.lib()
-        flags = _flags(early_stop, precision)
+        flags = _flags(early_stop, precision, schedule)
         with self._lock:
             for c0 in range(0, B, self.max_batch):
                 c1 = min(B, c0 + self.max_batch)
@@ -382,7 +392,8 @@ class ParallelDecoder:
         return res
 
     def decode_priors_async(self, P, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
-                            out: BatchResult | None = None, precision: str = "fp64") -> "PendingDecode":
+                            out: BatchResult | None = None, precision: str = "fp64",
+                            schedule: str = "auto") -> "PendingDecode":
         """Streaming variant of decode_priors (no reference counterpart): enqueue the H2D copy,
         the decode and the D2H copy of one batch (B <= max_batch) and return at once; call
         ``.wait()`` on the result for the BatchResult.  Two batches can be in flight, so the
@@ -405,7 +416,7 @@ class ParallelDecoder:
         ticket = ctypes.c_int64(-1)
         with self._lock:
             rc = _native.lib().ldpc_decoder_submit(
-                self._h, P.ctypes.data, B, int(max_iterations), _flags(early_stop, precision),
+                self._h, P.ctypes.data, B, int(max_iterations), _flags(early_stop, precision, schedule),
                 res.est_bits.ctypes.data, res.success.ctypes.data, res.iterations.ctypes.data,
                 res.syn_bits.ctypes.data, ctypes.byref(ticket))
             if rc == _native.LDPC_ECUDA or rc == _native.LDPC_ECLOSED:
@@ -435,7 +446,7 @@ class ParallelDecoder:
 
     def decode_device(self, P_dev, max_iterations: int, early_stop: bool = True, workspace=None,
                       outputs=None, profile: "_native.Profile | None" = None, syndrome_out: bool = True,
-                      precision: str = "fp64"):
+                      precision: str = "fp64", schedule: str = "auto"):
         """Device priors tensor [B, n] fp64 -> device tensors (est_bits, success, iters, syn_bits).
 
         Stream-ordered on torch's current stream; no host synchronisation
@@ -455,7 +466,7 @@ class ParallelDecoder:
         if outputs is None:
             outputs = self.alloc_outputs(B, P_dev.device)
         est, ok, its, syn = outputs
-        flags = _flags(early_stop, precision)
+        flags = _flags(early_stop, precision, schedule)
         rc = _native.lib().ldpc_decode(g.handle, _ptr(P_dev), B, int(max_iterations), flags, _ptr(est), _ptr(ok),
                                        _ptr(its), _ptr(syn) if syndrome_out else None, _ptr(workspace), nb,
                                        _native.current_stream_handle(),

@@ -29,6 +29,31 @@ __global__ void k_stream(double *msg, int E, int m, int dc) {
     }
 }
 
+// split layout: read D contiguous rows (own slots ni*D+i) of `src`, write them to scattered slots of `dst`
+template <int D>
+__global__ void k_split(const double *src, double *dst, const double *P, const int *slots, int E, int n, int cnt,
+                        int node0, int base) {
+    const int lane = threadIdx.x & 31;
+    const int ch = blockIdx.y;
+    const int ni = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (ni >= cnt) return;
+    const double2 *sb = reinterpret_cast<const double2 *>(src + (size_t)ch * E * C) + lane;
+    double2 *db = reinterpret_cast<double2 *>(dst + (size_t)ch * E * C) + lane;
+    const double2 *pb = reinterpret_cast<const double2 *>(P + (size_t)ch * n * C) + lane;
+    int s[D];
+#pragma unroll
+    for (int i = 0; i < D; i++) s[i] = __ldg(slots + (size_t)ni * D + i);
+    double2 p = __ldg(pb + (size_t)(node0 + ni) * (C / 2));
+    double2 v[D];
+#pragma unroll
+    for (int i = 0; i < D; i++) v[i] = __ldcs(sb + (size_t)(base + ni * D + i) * (C / 2));
+#pragma unroll
+    for (int i = 0; i < D; i++) {
+        v[i].x += p.x;
+        __stcs(db + (size_t)s[i] * (C / 2), v[i]);
+    }
+}
+
 template <int D>
 __global__ void k_gather(double *msg, const double *P, const int *slots, int E, int n, int cnt, int node0) {
     const int lane = threadIdx.x & 31;
@@ -94,6 +119,22 @@ int main(int argc, char **argv) {
     });
     run("gather var deg2", (2.0 * n2 * 2 + n2) * row * chunks, [&] {
         k_gather<2><<<dim3((n2 + 7) / 8, chunks), 256>>>(msg, P, s2, E, n, n2, n8 + n3);
+    });
+    double *msg2;
+    cudaMalloc(&msg2, (size_t)E * B * 8);
+    cudaMemset(msg2, 0, (size_t)E * B * 8);
+    run("split var deg8 (rd contig, wr scat)", (2.0 * n8 * 8 + n8) * row * chunks, [&] {
+        k_split<8><<<dim3((n8 + 7) / 8, chunks), 256>>>(msg, msg2, P, s8, E, n, n8, 0, 0);
+    });
+    run("split var deg3", (2.0 * n3 * 3 + n3) * row * chunks, [&] {
+        k_split<3><<<dim3((n3 + 7) / 8, chunks), 256>>>(msg, msg2, P, s3, E, n, n3, n8, n8 * 8);
+    });
+    run("split var deg2", (2.0 * n2 * 2 + n2) * row * chunks, [&] {
+        k_split<2><<<dim3((n2 + 7) / 8, chunks), 256>>>(msg, msg2, P, s2, E, n, n2, n8 + n3, n8 * 8 + n3 * 3);
+    });
+    // check-like with scattered writes: read 7 contiguous rows, write them to a random permutation
+    run("split check deg7 (rd contig, wr scat)", 2.0 * E * row * chunks, [&] {
+        k_split<7><<<dim3((m + 7) / 8, chunks), 256>>>(msg, msg2, P, slots, E, n, m, 0, 0);
     });
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;

@@ -1,10 +1,6 @@
-# env-selected kernel variants, device-timed bench (no e2e/cpu/fast legs)
+# env-selected kernel variants, device-timed bench (no e2e/cpu/fast legs); usage: bash tools/variant_probe.sh "ENV=.. ENV2=.." ...
 run() {
   env $1 timeout 300 python bench.py --no-e2e --no-cpu --no-fast --steps 20 --warmup 3 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$1'.ljust(28), 'ms', round(d['ms_per_step'],3), 'Gbit/s', round(d['value'],3), {k: round(v,3) for k,v in r['kernel_ms_per_step'].items()})"
+import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$1'.ljust(44), 'ms', round(d['ms_per_step'],3), 'Gbit/s', round(d['value'],3), {k: round(v,3) for k,v in r['kernel_ms_per_step'].items()})"
 }
-run X=0
-run LDPC_RING_MINB=3
-run LDPC_RING_MINB=4
-run LDPC_KERNEL=reg
-run X=0
+for v in "$@"; do run "$v"; done
