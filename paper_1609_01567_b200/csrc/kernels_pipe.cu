@@ -49,35 +49,6 @@ struct Ring {
     static constexpr size_t kBytes = kIdsBytes + (size_t)S * ROWS * 32 * V * sizeof(double);
 };
 
-// The (chunk, node) of a warp's successive tasks t, t + W, t + 2W, ... (chunk-major
-// order t = ch * node_count + ni), advanced without a division per task.
-struct TaskCursor {
-    int ch, ni, dq, dr, nc;
-    __device__ __forceinline__ TaskCursor(int64_t t, int64_t W, int nc_) : nc(nc_) {
-        ch = (int)(t / nc);
-        ni = (int)(t - (int64_t)ch * nc);
-        dq = (int)(W / nc);
-        dr = (int)(W - (int64_t)dq * nc);
-    }
-    __device__ __forceinline__ void next() {
-        ni += dr;
-        ch += dq;
-        if (ni >= nc) {
-            ni -= nc;
-            ch += 1;
-        }
-    }
-};
-
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 template <int V>
 __device__ __forceinline__ void st_v(double *p, const double (&o)[V]) {
