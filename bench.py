@@ -82,6 +82,16 @@ def workload_desc(cfg, H, B, iters, ebno):
 
 # ---- CPU reference (oracle port of the reference decoder, test-infrastructure) ----
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
 def cpu_reference_rate(H, P, iters, seconds):
     """Time the oracle (C restatement of serial.py) on host threads: (Gbit/s, cores, frames, secs)."""
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -137,7 +147,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"each step {len(P)} frames of the workload's code (fixed {iters} iterations) "
                                    f"decoded by the C restatement of the reference decoder (oracle/) on "
-                                   f"{cores} host threads"},
+                                   f"{cores} host threads ({cpu_model()})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -377,7 +387,7 @@ def run_ours(args):
         v, cores, frames, secs = cpu_reference_rate(H, P_host, iters, args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{frames} frames of the workload (fixed {iters} iterations) in {secs:.1f} s by the C "
-                         f"restatement of the reference decoder (oracle/) on {cores} host threads"}
+                         f"restatement of the reference decoder (oracle/) on {cores} host threads ({cpu_model()})"}
 
     if rank == 0:
         line = {
