@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-fast", action="store_true", help="skip the fp32 fast-mode leg")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other-BASELINE-configs leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--sub-batch", type=int, default=0, help="e2e pipeline sub-batch (0 = decoder default)")
     return ap.parse_args()
@@ -382,6 +383,34 @@ def run_ours(args):
                 "identical_frames_vs_f64": same,
                 "note": "f4 fast mode: same algorithm in fp32 (not bit-exact; tolerance in DESIGN.md)"}
 
+    # the other BASELINE.json configs (parity-test cases, reported for reference, not the headline):
+    # device-timed decode per call through decode_device with the automatic schedule
+    others = None
+    if world == 1 and not args.no_configs and cfg == "C3":
+        others = {}
+        for name, B_o, it_o, early_o in (("C1", 1, 50, True), ("C2", 4096, 20, False), ("C4", 256, 20, True)):
+            H_o = configs.code(name)
+            T_o = CodeTables.from_matrix(H_o)
+            P_o = torch.from_numpy(synthetic_priors(H_o, B_o, args.ebno, seed=5)[0]).to(dev)
+            with ParallelDecoder(T_o, max_batch=B_o) as d_o:
+                ws_o, outs_o = d_o.workspace(B_o), d_o.alloc_outputs(B_o, dev)
+                for _ in range(3):
+                    d_o.decode_device(P_o, it_o, early_stop=early_o, workspace=ws_o, outputs=outs_o)
+                reps = 20 if B_o < 64 else 5
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(stream)
+                for _ in range(reps):
+                    d_o.decode_device(P_o, it_o, early_stop=early_o, workspace=ws_o, outputs=outs_o)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms_o = e0.elapsed_time(e1) / reps
+                its_o = outs_o[2].float().mean().item()
+            others[name] = {"batch": B_o, "max_iterations": it_o, "early_stop": early_o, "ms_per_decode": ms_o,
+                            "coded_Gbit_s": B_o * H_o.n / (ms_o / 1e3) / 1e9, "mean_iterations": its_o,
+                            "n": H_o.n, "edges": H_o.total_edges}
+            del P_o, ws_o, outs_o
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, frames, secs = cpu_reference_rate(H, P_host, iters, args.cpu_seconds)
@@ -408,6 +437,7 @@ def run_ours(args):
             "e2e": e2e,
             "e2e_stream": e2e_stream,
             "fast_fp32": fast,
+            "other_configs": others,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "counts": {"bit_errors": int(counts[0]), "failures": int(counts[1]), "iterations": int(counts[2]),
