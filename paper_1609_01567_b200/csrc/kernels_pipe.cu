@@ -95,7 +95,10 @@ __device__ __forceinline__ int load_id(const NodeLaunch &a, int ni, int lane) {
 // Variables of degree >= kPriorRegDeg fetch their prior row into registers one
 // iteration ahead (their iterations are long enough to hide the latency, and the
 // smaller ring gains a stage); lower degrees stage the prior row in the ring.
-constexpr int kPriorRegDeg = 6;
+#ifndef LDPC_PRIOR_REG_DEG
+#define LDPC_PRIOR_REG_DEG 6
+#endif
+constexpr int kPriorRegDeg = LDPC_PRIOR_REG_DEG;
 template <int D, bool IS_VAR>
 constexpr bool prior_in_ring() { return IS_VAR && D < kPriorRegDeg; }
 template <int D, bool IS_VAR>

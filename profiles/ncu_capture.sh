@@ -6,7 +6,7 @@ set -u
 TAG=${1:-r1}
 OUT=gpurun_out
 mkdir -p $OUT
-BENCH="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu"
+BENCH="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-configs"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(check|var|node|syndrome|update|transpose|pack|finalize|count|fill)" -c 120 --csv \
     --log-file $OUT/launches_$TAG.csv $BENCH > $OUT/ncu_launches_$TAG.log 2>&1
 echo "launch list rc=$?"

@@ -5,7 +5,7 @@ i=0
 for v in "$@"; do
   i=$((i+1))
   env $v timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv \
-     --log-file gpurun_out/lp_$i.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-fast > /dev/null 2>&1
+     --log-file gpurun_out/lp_$i.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-fast --no-configs > /dev/null 2>&1
   python - "$v" gpurun_out/lp_$i.csv <<'PY'
 import csv, sys, collections, statistics
 rows = [r for r in csv.DictReader(l for l in open(sys.argv[2]) if l.startswith('"'))]
