@@ -72,3 +72,28 @@ def test_onchip_refuses_codes_that_do_not_fit(cuda):
             dec.decode_priors(_priors(H, 1, 2.0, seed=1), 2, schedule="onchip")
         with pytest.raises(ValueError):
             dec.decode_priors(_priors(H, 1, 2.0, seed=1), 2, schedule="sideways")
+
+
+def test_random_codes_all_schedules(cuda):
+    # random valid H (every row and column non-empty; degree-1 nodes, dense rows past the
+    # register-path degrees), both schedules, both stop modes, against the oracle
+    from conftest import random_parity_matrix
+    from oracle import OracleTables
+
+    rng = np.random.default_rng(2024)
+    for case in range(12):
+        H = random_parity_matrix(rng, max_m=48, max_n=96)
+        B = int(rng.integers(1, 40))
+        it = int(rng.integers(0, 12))
+        early = bool(case % 2)
+        P = rng.uniform(size=(B, H.n))
+        P[rng.uniform(size=P.shape) < 0.05] = 0.0   # saturated priors (serial.py:49 overflow)
+        P[rng.uniform(size=P.shape) < 0.05] = 1.0
+        est, ok, its, z = OracleTables.from_matrix(H).decode_batch(P, it, fixed_iterations=not early)
+        with ParallelDecoder(CodeTables.from_matrix(H), max_batch=B) as dec:
+            for sched in ("stream", "onchip"):
+                r = dec.decode_priors(P, it, early_stop=early, schedule=sched)
+                assert np.array_equal(r.estimates(), est), (case, sched)
+                assert np.array_equal(r.syndromes(), z), (case, sched)
+                assert np.array_equal(r.success.astype(bool), ok), (case, sched)
+                assert np.array_equal(r.iterations, its), (case, sched)
