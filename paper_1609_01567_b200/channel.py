@@ -85,6 +85,22 @@ def derive_state(*keys: int) -> RngState:
 
 # ---- channel.py:31-67 -------------------------------------------------------
 
+def shuffle(items: list, state: RngState) -> RngState:
+    """rng.py:84-90: Fisher-Yates from the last position down; the partner of position i is the
+    high 64 bits of x * (i + 1) for the next output x.  In place; returns the advanced state."""
+    for i in range(len(items) - 1, 0, -1):
+        state, x = rng_next(state)
+        j = (x * (i + 1)) >> 64
+        items[i], items[j] = items[j], items[i]
+    return state
+
+
+def randrange(state: RngState, bound: int) -> tuple[RngState, int]:
+    """rng.py:93-96: an integer in [0, bound), the high 64 bits of x * bound."""
+    state, x = rng_next(state)
+    return state, (x * bound) >> 64
+
+
 def box_muller(u1: float, u2: float) -> tuple[float, float]:
     """Standard normal pair from two uniforms, u1 in (0, 1] (channel.py:31-37)."""
     if u1 <= 0.0:

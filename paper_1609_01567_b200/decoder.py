@@ -294,6 +294,75 @@ class BatchResult:
 
 # ---- the decoder ----------------------------------------------------------------
 
+# ---- engine.py's page plan and shared-state phase API (engine.py:33-76, 157-190) ------------
+# The reference sweeps pages of `group_size` lanes with worker threads; here the CUDA grid
+# replaces the pages, so the plan is kept for API compatibility (results do not depend on it,
+# in the reference either) and the parallel_* entry points run the GPU phase kernels on the
+# state's arrays, writing their outputs in place like the reference.
+
+@dataclass(frozen=True)
+class PagePlan:
+    """engine.py:33-47: split of total_edges lanes into pages of at most group_size."""
+
+    total_edges: int
+    group_size: int
+    page_starts: tuple
+
+    @property
+    def page_count(self) -> int:
+        return len(self.page_starts)
+
+    def page_width(self, page: int) -> int:
+        """Active lanes in a page; trailing lanes of the last page idle."""
+        return min(self.group_size, self.total_edges - self.page_starts[page])
+
+
+def plan_pages(total_edges: int, group_size: int) -> PagePlan:
+    """engine.py:50-55, same errors."""
+    if group_size < 1:
+        raise ValueError("group_size must be at least 1")
+    if total_edges < 1:
+        raise ValueError("total_edges must be at least 1")
+    return PagePlan(total_edges, group_size, tuple(range(0, total_edges, group_size)))
+
+
+@dataclass
+class SharedDecodeState:
+    """engine.py:58-76: the arrays one decode works on (host numpy, updated in place)."""
+
+    p: np.ndarray          # n priors
+    q: np.ndarray          # E variable-to-check messages
+    r: np.ndarray          # E check-to-variable messages
+    estimate: np.ndarray   # n hard bits
+    syndrome: np.ndarray   # m parity bits
+
+    @classmethod
+    def allocate(cls, tables) -> "SharedDecodeState":
+        T = _tables_of(tables)
+        return cls(p=np.zeros(T.n), q=np.zeros(T.total_edges), r=np.full(T.total_edges, 0.5),
+                   estimate=np.zeros(T.n, dtype=np.uint8), syndrome=np.zeros(T.m, dtype=np.uint8))
+
+
+def parallel_to_check(state: SharedDecodeState, tables, plan: PagePlan | None = None) -> None:
+    """engine.py:157-163: variable-to-check update on the GPU; writes state.q."""
+    state.q[...] = values_to_check(state.p, state.r, tables)
+
+
+def parallel_to_variable(state: SharedDecodeState, tables, plan: PagePlan | None = None) -> None:
+    """engine.py:166-172: check-to-variable update on the GPU; writes state.r."""
+    state.r[...] = values_to_variable(state.q, tables)
+
+
+def parallel_estimate(state: SharedDecodeState, tables, plan: PagePlan | None = None) -> None:
+    """engine.py:175-181: hard decision on the GPU; writes state.estimate."""
+    state.estimate[...] = estimate(state.p, state.r, tables)
+
+
+def parallel_syndrome(state: SharedDecodeState, tables, plan: PagePlan | None = None) -> None:
+    """engine.py:184-190: syndrome on the GPU; writes state.syndrome."""
+    state.syndrome[...] = syndrome(state.estimate, tables)
+
+
 class PendingDecode:
     """One in-flight ParallelDecoder.decode_priors_async batch; keeps its host buffers alive."""
 

@@ -62,3 +62,30 @@ def test_dense_format_round_trip_and_errors():
         parse_dense("011\n\n10\n")
     with pytest.raises(CodeFormatError, match="line 1: empty matrix"):
         parse_dense("\n \n")
+
+
+def test_gallager_generator_matches_reference_golden():
+    # codes.py:241-294 + rng.py:84-96, against fixtures made by running the reference
+    import pathlib
+
+    from paper_1609_01567_b200 import generate_gallager_code
+    from paper_1609_01567_b200.channel import derive_state, randrange, shuffle
+
+    g = np.load(pathlib.Path(__file__).with_name("golden") / "gallager.npz")
+    for k in range(int(g["cases"])):
+        n, wc, wr, seed = (int(x) for x in g[f"g{k}/params"])
+        H = generate_gallager_code(n, wc, wr, seed)
+        assert np.array_equal(np.array(H.ones, dtype=np.int64).reshape(-1, 2), g[f"g{k}/ones"]), (n, wc, wr, seed)
+    st = derive_state(5, 6, 7)
+    items = list(range(50))
+    st2 = shuffle(items, st)
+    st3, draws = st2, []
+    for b in (1, 2, 7, 1000, 2**40 + 3):
+        st3, v = randrange(st3, b)
+        draws.append(v)
+    assert [st.s0, st.s1, st2.s0, st2.s1, st3.s0, st3.s1] == [int(x) for x in g["rng/state"]]
+    assert items == [int(x) for x in g["rng/shuffled"]] and draws == [int(x) for x in g["rng/draws"]]
+    with pytest.raises(ValueError):
+        generate_gallager_code(10, 1, 2)
+    with pytest.raises(ValueError):
+        generate_gallager_code(10, 3, 7)
