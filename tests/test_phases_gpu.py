@@ -204,3 +204,35 @@ def test_unbounded_degree_phases_and_decode(cuda):
     est, ok, its, z = O.decode_batch(Pd, 2, fixed_iterations=True)
     assert np.array_equal(res.estimates(), est) and np.array_equal(res.syndromes(), z)
     assert np.array_equal(res.success.astype(bool), ok) and np.array_equal(res.iterations, its)
+
+
+def test_engine_shared_state_phases(cuda):
+    # engine.py:33-76, 157-190: plan_pages / SharedDecodeState / parallel_* write the state in place,
+    # equal to the single-phase functions and the oracle, for any page plan
+    from oracle import OracleTables
+    from paper_1609_01567_b200 import (SharedDecodeState, parallel_estimate, parallel_syndrome, parallel_to_check,
+                                       parallel_to_variable, plan_pages)
+
+    H = configs.code("C1")
+    T = CodeTables.from_matrix(H)
+    O = OracleTables.from_matrix(H)
+    rng = np.random.default_rng(8)
+    with pytest.raises(ValueError):
+        plan_pages(10, 0)
+    with pytest.raises(ValueError):
+        plan_pages(0, 4)
+    for group in (1, 7, 512):
+        plan = plan_pages(T.total_edges, group)
+        assert plan.page_count == -(-T.total_edges // group) and plan.page_width(plan.page_count - 1) >= 1
+        st = SharedDecodeState.allocate(T)
+        st.p[:] = rng.uniform(size=H.n)
+        st.q[:] = st.p[T.variable.v]                      # serial.py:58
+        q_id = st.q
+        parallel_to_variable(st, T, plan)
+        assert np.array_equal(bits(st.r), bits(O.values_to_variable(st.q)))
+        parallel_to_check(st, T, plan)
+        assert st.q is q_id and np.array_equal(bits(st.q), bits(O.values_to_check(st.p, st.r)))
+        parallel_estimate(st, T, plan)
+        assert np.array_equal(st.estimate, O.estimate(st.p, st.r))
+        parallel_syndrome(st, T, plan)
+        assert np.array_equal(st.syndrome, O.syndrome(st.estimate))
