@@ -1,13 +1,15 @@
 #!/bin/bash
 # Capture ncu evidence for the bench workload (run under gpurun, 1 GPU).
-#   launches_<tag>.csv : every kernel launch of one decode step with its device time
-#   prof_<tag>_*.ncu-rep : --set full captures of the top kernels
+#   launches_<tag>.csv       : every kernel launch of one bench step (C3) with its device time
+#   prof_<tag>_var/check     : --set full captures of the top kernels (variable rings, check)
+#   prof_<tag>_c4            : --set full of the high-degree chains kernels (C4: fp64-pipe bound)
+#   prof_<tag>_onchip        : --set full of the on-chip decoder (C1, one frame)
 set -u
 TAG=${1:-r1}
 OUT=gpurun_out
 mkdir -p $OUT
-BENCH="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-configs"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(check|var|node|syndrome|update|transpose|pack|finalize|count|fill)" -c 120 --csv \
+BENCH="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-configs --no-fast"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" -c 200 --csv \
     --log-file $OUT/launches_$TAG.csv $BENCH > $OUT/ncu_launches_$TAG.log 2>&1
 echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(var_reg|node_ring)" -s 3 -c 3 \
@@ -16,4 +18,12 @@ echo "var capture rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_check_reg -s 1 -c 1 \
     -o $OUT/prof_${TAG}_check $BENCH > $OUT/ncu_check_$TAG.log 2>&1
 echo "check capture rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_(check|var)_chains" -s 2 -c 2 \
+    -o $OUT/prof_${TAG}_c4 python bench.py --config C4 --iters 20 --steps 1 --warmup 0 --no-e2e --no-cpu \
+    --no-configs --no-fast > $OUT/ncu_c4_$TAG.log 2>&1
+echo "c4 capture rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_onchip -s 2 -c 1 \
+    -o $OUT/prof_${TAG}_onchip python bench.py --config C1 --batch 1 --iters 50 --steps 1 --warmup 0 --no-e2e \
+    --no-cpu --no-configs --no-fast > $OUT/ncu_onchip_$TAG.log 2>&1
+echo "onchip capture rc=$?"
 ls -la $OUT
