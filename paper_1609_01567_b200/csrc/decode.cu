@@ -201,6 +201,19 @@ NodeLaunch var_args(const ldpc_graph *g, const Workspace &w, const uint32_t *don
 float *msg32(const ldpc_graph *g, const Workspace &w) { return reinterpret_cast<float *>(w.msg); }
 float *prior32(const ldpc_graph *g, const Workspace &w) { return reinterpret_cast<float *>(w.msg) + (size_t)g->E * w.Bp; }
 
+// Alternating sweep direction: each node kernel sweeps the codeword chunks opposite to the
+// kernel before it, so it starts on the chunk whose rows the previous kernel touched last and
+// finds part of them in L2 (C3 step 14.16 -> 14.02 ms with default-caching hints;
+// profiles/r1_kernel_choice.md).  LDPC_ALT_SWEEP=0 disables it.
+static bool alt_sweep() {
+    static const bool on = [] {
+        const char *e = getenv("LDPC_ALT_SWEEP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+static thread_local int g_sweep = 0;  // direction of the next node-kernel launch
+
 int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const uint32_t *done, cudaStream_t s,
                 bool fast = false) {
     NodeLaunch a = check_args(g, w, done);
@@ -220,6 +233,7 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
+            a.reverse = alt_sweep() ? ((g_sweep ^= 1) ^ 1) : 0;
             int rc = use_ring(false, b.deg) ? launch_check_pipe(a, b.deg, from_prior, s)
                                         : launch_check_bucket(a, b.deg, from_prior, s);
             if (rc) return rc;
@@ -256,6 +270,7 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
+            a.reverse = alt_sweep() ? ((g_sweep ^= 1) ^ 1) : 0;
             int rc = use_ring(true, b.deg) ? launch_var_pipe(a, b.deg, write_q, s)
                                         : launch_var_bucket(a, b.deg, write_q, s);
             if (rc) return rc;

@@ -293,12 +293,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int6
     // issued), so the index loads' L2 latency is off the critical path; the
     // cursor runs two tasks ahead of the issue.
     TaskCursor cur(first, W, a.node_count);
-    int nid0 = load_id<D, IS_VAR, FP>(a, cur.ni, lane), nch0 = cur.ch;
+    const int chunks_m1 = a.Bp / (32 * V) - 1;  // reverse sweep: chunk c -> chunks-1-c
+    auto chunk_of = [&](int c) { return a.reverse ? chunks_m1 - c : c; };
+    int nid0 = load_id<D, IS_VAR, FP>(a, cur.ni, lane), nch0 = chunk_of(cur.ch);
     cur.next();
     int nid1 = 0, nch1 = 0;
     if (ntask > 1) {
         nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
-        nch1 = cur.ch;
+        nch1 = chunk_of(cur.ch);
         cur.next();
     }
     auto issue_next = [&](int j) {  // issue task j (j < ntask) into stage j % S
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int6
         nch0 = nch1;
         if (j + 2 < ntask) {
             nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
-            nch1 = cur.ch;
+            nch1 = chunk_of(cur.ch);
             cur.next();
         }
         const int sj = j % S;
