@@ -312,6 +312,7 @@ int init_flags(const Workspace &w, bool early, cudaStream_t s) {
 // (streaming schedule) or one tile (tiled schedule).
 static int decode_view(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s,
                        Prof &prof, bool fast) {
+    g_sweep = 0;  // every decode (and so every captured graph) uses the same direction sequence
     const int64_t B = w.B, E = g->E, n = g->n, m = g->m;
     const int64_t wb = fast ? 4 : 8;                         // message / prior width in bytes
     const int64_t c_bytes = 2 * wb * E * B;                  // read q (or p-gather) + write r
