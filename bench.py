@@ -232,9 +232,17 @@ def run_ours(args):
     from paper_1609_01567_b200 import CodeTables, ParallelDecoder, _native, configs
 
     rank, local_rank, world = dist_env()
+    # LDPC_BENCH_ONE_GPU=1 (testing the multi-rank flow on a one-GPU box): every rank on cuda:0,
+    # gloo instead of NCCL (NCCL refuses two ranks on one device).  Never used for reported numbers.
+    one_gpu = os.environ.get("LDPC_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
     if world > 1:
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     dev = torch.device(f"cuda:{local_rank}")
     torch.cuda.set_device(dev)
     cfg = args.config
