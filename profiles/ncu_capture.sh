@@ -22,7 +22,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_(
     -o $OUT/prof_${TAG}_c4 python bench.py --config C4 --iters 20 --steps 1 --warmup 0 --no-e2e --no-cpu \
     --no-configs --no-fast > $OUT/ncu_c4_$TAG.log 2>&1
 echo "c4 capture rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_onchip -s 2 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_onchip -s 0 -c 1 \
     -o $OUT/prof_${TAG}_onchip python bench.py --config C1 --batch 1 --iters 50 --steps 1 --warmup 0 --no-e2e \
     --no-cpu --no-configs --no-fast > $OUT/ncu_onchip_$TAG.log 2>&1
 echo "onchip capture rc=$?"
