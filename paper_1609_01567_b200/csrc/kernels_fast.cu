@@ -16,6 +16,8 @@
 namespace ldpc {
 namespace {
 
+// fp32 mode keeps evict-first hints and a forward sweep (measured faster than default caching
+// with the alternating sweep the fp64 kernels use: 7.9 vs 7.7-7.8 Gbit/s)
 __device__ __forceinline__ float2 ld2(const float *p) { return __ldcs(reinterpret_cast<const float2 *>(p)); }
 __device__ __forceinline__ void st2(float *p, float x, float y) {
     __stcs(reinterpret_cast<float2 *>(p), make_float2(x, y));
@@ -24,16 +26,16 @@ __device__ __forceinline__ void st2(float *p, float x, float y) {
 template <int D, bool FROM_PRIOR>
 __global__ void __launch_bounds__(kThreads) k_check_f32(NodeLaunch a, float *msg, const float *P) {
     const int lane = threadIdx.x & 31;
-    const int chunks = a.Bp / 64;
-    const int64_t task = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    const int ch = (int)(task / a.node_count);
-    const int ni = (int)(task - (int64_t)ch * a.node_count);
-    if (ch >= chunks) return;
+    // grid (node blocks, codeword chunks), dispatched x-fastest: chunk-major sweep
+    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int ni = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (ni >= a.node_count) return;
     if (a.done != nullptr) {
         const uint2 d = *reinterpret_cast<const uint2 *>(a.done + 2 * ch);
         if ((d.x & d.y) == 0xffffffffu) return;
     }
-    const int cw = ch * 64 + 2 * lane;
+    float *mb = chunk_base(msg, a.msg_rows, ch * 64) + 2 * lane;
+    const float *pb = chunk_base(P, a.p_rows, ch * 64) + 2 * lane;
     const int32_t base = a.edge_begin + ni * D;
     int slot[D];
 #pragma unroll
@@ -41,8 +43,8 @@ __global__ void __launch_bounds__(kThreads) k_check_f32(NodeLaunch a, float *msg
     float b[D][2];
 #pragma unroll
     for (int i = 0; i < D; i++) {
-        const float2 q = FROM_PRIOR ? *reinterpret_cast<const float2 *>(P + cofs(a.p_rows, __ldg(a.var_ord + base + i), cw))
-                                    : ld2(msg + cofs(a.msg_rows, slot[i], cw));
+        const float2 q = FROM_PRIOR ? *reinterpret_cast<const float2 *>(pb + row_off(__ldg(a.var_ord + base + i)))
+                                    : ld2(mb + row_off(slot[i]));
         b[i][0] = __fsub_rn(1.0f, __fmul_rn(2.0f, q.x));
         b[i][1] = __fsub_rn(1.0f, __fmul_rn(2.0f, q.y));
     }
@@ -55,7 +57,7 @@ __global__ void __launch_bounds__(kThreads) k_check_f32(NodeLaunch a, float *msg
             a0 = __fmul_rn(a0, b[i][0]);
             a1 = __fmul_rn(a1, b[i][1]);
         }
-        st2(msg + cofs(a.msg_rows, slot[k], cw), __fsub_rn(1.0f, __fadd_rn(0.5f, __fmul_rn(0.5f, a0))),
+        st2(mb + row_off(slot[k]), __fsub_rn(1.0f, __fadd_rn(0.5f, __fmul_rn(0.5f, a0))),
             __fsub_rn(1.0f, __fadd_rn(0.5f, __fmul_rn(0.5f, a1))));
         if (k + 1 < D) {
             pre0 = __fmul_rn(pre0, b[k][0]);
@@ -67,26 +69,26 @@ __global__ void __launch_bounds__(kThreads) k_check_f32(NodeLaunch a, float *msg
 template <int D, bool WRITE_Q>
 __global__ void __launch_bounds__(kThreads) k_var_f32(NodeLaunch a, float *msg, const float *P) {
     const int lane = threadIdx.x & 31;
-    const int chunks = a.Bp / 64;
-    const int64_t task = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    const int ch = (int)(task / a.node_count);
-    const int ni = (int)(task - (int64_t)ch * a.node_count);
-    if (ch >= chunks) return;
+    // grid (node blocks, codeword chunks), dispatched x-fastest: chunk-major sweep
+    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int ni = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (ni >= a.node_count) return;
     if (a.done != nullptr) {
         const uint2 d = *reinterpret_cast<const uint2 *>(a.done + 2 * ch);
         if ((d.x & d.y) == 0xffffffffu) return;
     }
-    const int cw = ch * 64 + 2 * lane;
+    float *mb = chunk_base(msg, a.msg_rows, ch * 64) + 2 * lane;
+    const float *pb = chunk_base(P, a.p_rows, ch * 64) + 2 * lane;
     const int node = __ldg(a.order + a.node_begin + ni);
     const int32_t base = a.edge_begin + ni * D;
     int pos[D];
 #pragma unroll
     for (int i = 0; i < D; i++) pos[i] = __ldg(a.slot_ord + base + i);
-    const float2 pj = *reinterpret_cast<const float2 *>(P + cofs(a.p_rows, node, cw));
+    const float2 pj = *reinterpret_cast<const float2 *>(pb + row_off(node));
     float r[D][2], om[D][2];
 #pragma unroll
     for (int i = 0; i < D; i++) {
-        const float2 x = ld2(msg + cofs(a.msg_rows, pos[i], cw));
+        const float2 x = ld2(mb + row_off(pos[i]));
         r[i][0] = x.x;
         r[i][1] = x.y;
         om[i][0] = __fsub_rn(1.0f, x.x);
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(kThreads) k_var_f32(NodeLaunch a, float *msg, 
                 const float den = __fadd_rn(q0, q1);
                 out[v] = (den == 0.0f) ? 0.5f : __fdiv_rn(q1, den);
             }
-            st2(msg + cofs(a.msg_rows, pos[k], cw), out[0], out[1]);
+            st2(mb + row_off(pos[k]), out[0], out[1]);
         }
 #pragma unroll
         for (int v = 0; v < 2; v++) {
@@ -167,11 +169,11 @@ unsigned grid_of(int64_t work) {
 
 template <int D, bool FLAG, bool IS_VAR>
 int launch_f32(const NodeLaunch &a, float *msg, const float *P, cudaStream_t s) {
-    const int64_t tasks = (int64_t)a.node_count * (a.Bp / 64);
-    const int64_t blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    if (blocks == 0) return LDPC_OK;
-    if constexpr (IS_VAR) k_var_f32<D, FLAG><<<(unsigned)blocks, kThreads, 0, s>>>(a, msg, P);
-    else k_check_f32<D, FLAG><<<(unsigned)blocks, kThreads, 0, s>>>(a, msg, P);
+    if (a.node_count == 0) return LDPC_OK;
+    const dim3 grid((a.node_count + kWarpsPerBlock - 1) / kWarpsPerBlock, a.Bp / 64);
+    LDPC_ARG_CHECK(grid.y <= 65535u, "batch too large for one launch (%d codewords)", a.Bp);
+    if constexpr (IS_VAR) k_var_f32<D, FLAG><<<grid, kThreads, 0, s>>>(a, msg, P);
+    else k_check_f32<D, FLAG><<<grid, kThreads, 0, s>>>(a, msg, P);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }
