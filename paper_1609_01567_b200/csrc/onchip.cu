@@ -467,15 +467,16 @@ static int resident_ctas(const ldpc_graph *g) {
     return sms * per_sm;
 }
 
+static std::mutex g_res_mu;
+static std::map<const ldpc_graph *, int> g_resident;  // per graph; dropped by onchip_forget
+
 bool onchip_auto(const ldpc_graph *g, int32_t B) {
     if (onchip_cluster_size(g) != 1) return false;
-    static std::mutex mu;
-    static std::map<const ldpc_graph *, int> cache;
     int res;
     {
-        std::lock_guard<std::mutex> lock(mu);
-        auto it = cache.find(g);
-        if (it == cache.end()) it = cache.emplace(g, resident_ctas(g)).first;
+        std::lock_guard<std::mutex> lock(g_res_mu);
+        auto it = g_resident.find(g);
+        if (it == g_resident.end()) it = g_resident.emplace(g, resident_ctas(g)).first;
         res = it->second;
     }
     return B <= 2 * res;
@@ -552,6 +553,10 @@ int launch_onchip(const ldpc_graph *g, int CS, const double *p_dev, int32_t B, i
 }
 
 void onchip_forget(const ldpc_graph *g) {
+    {
+        std::lock_guard<std::mutex> lock(g_res_mu);
+        g_resident.erase(g);
+    }
     std::lock_guard<std::mutex> lock(g_plan_mu);
     for (auto it = g_plans.begin(); it != g_plans.end();) {
         if (it->first.first == g) {
