@@ -21,6 +21,7 @@
 
 namespace ldpc {
 
+
 namespace {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 }  // namespace
@@ -392,6 +393,7 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
                            uint32_t *syn_bits_dev, void *workspace_dev, size_t workspace_bytes_, void *stream,
                            ldpc_profile *prof_host) {
     LDPC_ARG_CHECK(g != nullptr, "NULL graph");
+    DeviceGuard dg(g->device);
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
     LDPC_ARG_CHECK(p_dev && est_bits_dev && success_dev && iters_dev, "NULL output/input pointer");
     LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32 | LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP)) == 0,
@@ -486,6 +488,7 @@ extern "C" int ldpc_decode_channel(const ldpc_graph *g, uint64_t seed, uint64_t 
                                    uint8_t *success_dev, int32_t *iters_dev, uint32_t *syn_bits_dev,
                                    void *workspace_dev, size_t workspace_bytes_, void *stream) {
     LDPC_ARG_CHECK(g != nullptr, "NULL graph");
+    DeviceGuard dg(g->device);
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
     LDPC_ARG_CHECK(sigma2 > 0.0, "sigma2 must be positive");
     LDPC_ARG_CHECK(est_bits_dev && success_dev && iters_dev, "NULL output pointer");
@@ -512,6 +515,7 @@ extern "C" int ldpc_decode_channel(const ldpc_graph *g, uint64_t seed, uint64_t 
 extern "C" int ldpc_count_errors(const ldpc_graph *g, const uint32_t *est_bits_dev, const uint8_t *success_dev,
                                  const int32_t *iters_dev, int32_t B, int64_t *counts_dev, void *stream) {
     LDPC_ARG_CHECK(g && est_bits_dev && success_dev && iters_dev && counts_dev, "NULL argument");
+    DeviceGuard dg(g->device);
     LDPC_ARG_CHECK(B >= 1, "batch must be at least 1");
     return launch_count_errors(est_bits_dev, (g->n + 31) / 32, success_dev, iters_dev, B, counts_dev,
                                (cudaStream_t)stream);
@@ -521,6 +525,7 @@ extern "C" int ldpc_count_errors(const ldpc_graph *g, const uint32_t *est_bits_d
 extern "C" int ldpc_phase_to_variable(const ldpc_graph *g, const double *q_dev, double *r_dev, int32_t B,
                                       void *ws, size_t ws_bytes, void *stream) {
     LDPC_ARG_CHECK(g && q_dev && r_dev, "NULL argument");
+    DeviceGuard dg(g->device);
     Workspace w;
     int rc = carve_workspace(g, B, ws, ws_bytes, &w);
     if (rc) return rc;
@@ -533,6 +538,7 @@ extern "C" int ldpc_phase_to_variable(const ldpc_graph *g, const double *q_dev, 
 extern "C" int ldpc_phase_to_check(const ldpc_graph *g, const double *p_dev, const double *r_dev, double *q_dev,
                                    int32_t B, void *ws, size_t ws_bytes, void *stream) {
     LDPC_ARG_CHECK(g && p_dev && r_dev && q_dev, "NULL argument");
+    DeviceGuard dg(g->device);
     Workspace w;
     int rc = carve_workspace(g, B, ws, ws_bytes, &w);
     if (rc) return rc;
@@ -546,6 +552,7 @@ extern "C" int ldpc_phase_to_check(const ldpc_graph *g, const double *p_dev, con
 extern "C" int ldpc_phase_estimate(const ldpc_graph *g, const double *p_dev, const double *r_dev,
                                    uint8_t *chat_dev, int32_t B, void *ws, size_t ws_bytes, void *stream) {
     LDPC_ARG_CHECK(g && p_dev && r_dev && chat_dev, "NULL argument");
+    DeviceGuard dg(g->device);
     Workspace w;
     int rc = carve_workspace(g, B, ws, ws_bytes, &w);
     if (rc) return rc;
@@ -559,6 +566,7 @@ extern "C" int ldpc_phase_estimate(const ldpc_graph *g, const double *p_dev, con
 extern "C" int ldpc_phase_syndrome(const ldpc_graph *g, const uint8_t *chat_dev, uint8_t *z_dev, int32_t B,
                                    void *ws, size_t ws_bytes, void *stream) {
     LDPC_ARG_CHECK(g && chat_dev && z_dev, "NULL argument");
+    DeviceGuard dg(g->device);
     Workspace w;
     int rc = carve_workspace(g, B, ws, ws_bytes, &w);
     if (rc) return rc;
@@ -573,6 +581,7 @@ extern "C" int ldpc_phase_syndrome(const ldpc_graph *g, const uint8_t *chat_dev,
 extern "C" int ldpc_phase_f32(const ldpc_graph *g, int phase, const double *p_dev, const double *in_dev,
                               double *out_dev, int32_t B, void *ws, size_t ws_bytes, void *stream) {
     LDPC_ARG_CHECK(g && in_dev && out_dev && (phase == 1 || p_dev), "NULL argument");
+    DeviceGuard dg(g->device);
     LDPC_ARG_CHECK(phase == 0 || phase == 1, "phase must be 0 (to check) or 1 (to variable)");
     LDPC_ARG_CHECK(g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree,
                    "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
@@ -647,6 +656,7 @@ struct ldpc_decoder {
 
 static void decoder_free(ldpc_decoder *d) {
     if (!d) return;
+    DeviceGuard dg(d->g->device);
     for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_comp[2], d->s_comp[3], d->s_out})
         if (s) cudaStreamSynchronize(s);
     for (void *w : d->ws) cudaFree(w);
@@ -702,6 +712,7 @@ static std::vector<int32_t> chunk_plan(int32_t B, int32_t sub) {
 
 extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32_t sub_batch, ldpc_decoder **out) {
     LDPC_ARG_CHECK(g && out, "NULL argument");
+    DeviceGuard dg(g->device);
     LDPC_ARG_CHECK(max_batch >= 1, "max_batch must be at least 1");
     *out = nullptr;
     ldpc_decoder *d = new ldpc_decoder();
@@ -746,6 +757,7 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
         return LDPC_ECLOSED;
     }
     std::lock_guard<std::mutex> lock(d->mu);
+    DeviceGuard dg(d->g->device);
     if (d->poisoned) {
         set_error("decoder is closed after a device fault");
         return LDPC_ECLOSED;
@@ -842,6 +854,7 @@ extern "C" int ldpc_decoder_submit(ldpc_decoder *d, const double *p_host, int32_
         return LDPC_ECLOSED;
     }
     std::lock_guard<std::mutex> lock(d->mu);
+    DeviceGuard dg(d->g->device);
     if (d->poisoned) {
         set_error("decoder is closed after a device fault");
         return LDPC_ECLOSED;
@@ -901,6 +914,7 @@ extern "C" int ldpc_decoder_wait(ldpc_decoder *d, int64_t ticket) {
         return LDPC_ECLOSED;
     }
     std::lock_guard<std::mutex> lock(d->mu);
+    DeviceGuard dg(d->g->device);
     LDPC_ARG_CHECK(ticket >= 0 && ticket < d->next_ticket, "unknown ticket %lld", (long long)ticket);
     auto &sl = d->slots[ticket & 1];
     if (sl.ticket != ticket) return d->poisoned ? LDPC_ECLOSED : LDPC_OK;  // already collected

@@ -362,6 +362,7 @@ int build_ord(const int32_t *order, int32_t count, const int32_t *off, const int
 
 void free_graph(ldpc_graph *g) {
     if (!g) return;
+    DeviceGuard dg(g->device);
     onchip_forget(g);
     for (auto &kv : g->graphs)
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);

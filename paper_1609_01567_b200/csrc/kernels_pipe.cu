@@ -382,23 +382,29 @@ int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
     constexpr int ROWS = ring_rows<D, IS_VAR>();
     const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS, V, MINB>::kBytes;
     auto kern = k_node_ring<D, V, IS_VAR, FLAG, MINB>;
-    static int per_sm = -1, sms = 0;
+    // the shared-memory attribute is per device: set it (and size the grid) once per device
+    constexpr int kMaxDevices = 64;
+    static int per_sm_of[kMaxDevices] = {}, sms_of[kMaxDevices] = {};
     static std::mutex mu;
+    int dev = 0;
+    LDPC_CUDA_TRY(cudaGetDevice(&dev));
+    LDPC_ARG_CHECK(dev >= 0 && dev < kMaxDevices, "device ordinal %d out of range", dev);
+    int per_sm, sms;
     {
         std::lock_guard<std::mutex> lock(mu);
-        if (per_sm < 0) {
+        if (per_sm_of[dev] == 0) {
             LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            int dev = 0;
-            LDPC_CUDA_TRY(cudaGetDevice(&dev));
-            LDPC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            LDPC_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
             int b = 0;
             LDPC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kThreads, smem));
             if (b < 1) {
                 set_error("ring node kernel (degree %d) does not fit on an SM", D);
                 return LDPC_ECUDA;
             }
-            per_sm = b;
+            per_sm_of[dev] = b;
         }
+        per_sm = per_sm_of[dev];
+        sms = sms_of[dev];
     }
     const int64_t ntasks = (int64_t)a.node_count * (a.Bp / (32 * V));
     if (ntasks == 0) return LDPC_OK;
