@@ -131,7 +131,12 @@ def check(rc: int, what: str = "ldpc") -> None:
     raise RuntimeError(msg)
 
 
-def current_stream_handle():
+def current_stream_handle(device=None):
+    """torch's current stream on `device` (a graph's device index or torch device; default: current)."""
     import torch
 
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if device is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(device, int):
+        device = torch.device("cuda", device)
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)

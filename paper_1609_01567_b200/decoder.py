@@ -191,10 +191,10 @@ def values_to_check(p, r, tables: CodeTables, precision: str = "fp64") -> np.nda
     dq = torch.empty_like(dr)
     if precision == "fp32":
         rc = _native.lib().ldpc_phase_f32(g.handle, 0, _ptr(dp), _ptr(dr), _ptr(dq), B, _ptr(ws), nb,
-                                          _native.current_stream_handle())
+                                          _native.current_stream_handle(g.device))
     else:
         rc = _native.lib().ldpc_phase_to_check(g.handle, _ptr(dp), _ptr(dr), _ptr(dq), B, _ptr(ws), nb,
-                                               _native.current_stream_handle())
+                                               _native.current_stream_handle(g.device))
     _native.check(rc, "values_to_check")
     q = dq.cpu().numpy()
     return q[0] if single else q
@@ -213,10 +213,10 @@ def values_to_variable(q, tables: CodeTables, precision: str = "fp64") -> np.nda
     dr = torch.empty_like(dq)
     if precision == "fp32":
         rc = _native.lib().ldpc_phase_f32(g.handle, 1, None, _ptr(dq), _ptr(dr), B, _ptr(ws), nb,
-                                          _native.current_stream_handle())
+                                          _native.current_stream_handle(g.device))
     else:
         rc = _native.lib().ldpc_phase_to_variable(g.handle, _ptr(dq), _ptr(dr), B, _ptr(ws), nb,
-                                                  _native.current_stream_handle())
+                                                  _native.current_stream_handle(g.device))
     _native.check(rc, "values_to_variable")
     r = dr.cpu().numpy()
     return r[0] if single else r
@@ -234,7 +234,7 @@ def estimate(p, r, tables: CodeTables) -> np.ndarray:
     dp, dr = _dev(P, g.device), _dev(R, g.device)
     dc = torch.empty((B, T.n), dtype=torch.uint8, device=dp.device)
     _native.check(_native.lib().ldpc_phase_estimate(g.handle, _ptr(dp), _ptr(dr), _ptr(dc), B, _ptr(ws), nb,
-                                                    _native.current_stream_handle()), "estimate")
+                                                    _native.current_stream_handle(g.device)), "estimate")
     c = dc.cpu().numpy()
     return c[0] if single else c
 
@@ -255,7 +255,7 @@ def syndrome(c_hat, H) -> np.ndarray:
     dc = _dev(c2, g.device)
     dz = torch.empty((B, T.m), dtype=torch.uint8, device=dc.device)
     _native.check(_native.lib().ldpc_phase_syndrome(g.handle, _ptr(dc), _ptr(dz), B, _ptr(ws), nb,
-                                                    _native.current_stream_handle()), "syndrome")
+                                                    _native.current_stream_handle(g.device)), "syndrome")
     z = dz.cpu().numpy()
     return z[0] if single else z
 
@@ -538,7 +538,7 @@ class ParallelDecoder:
         flags = _flags(early_stop, precision, schedule)
         rc = _native.lib().ldpc_decode(g.handle, _ptr(P_dev), B, int(max_iterations), flags, _ptr(est), _ptr(ok),
                                        _ptr(its), _ptr(syn) if syndrome_out else None, _ptr(workspace), nb,
-                                       _native.current_stream_handle(),
+                                       _native.current_stream_handle(g.device),
                                        ctypes.byref(profile) if profile is not None else None)
         _native.check(rc, "ldpc_decode")
         return outputs
@@ -563,7 +563,7 @@ class ParallelDecoder:
         rc = _native.lib().ldpc_decode_channel(g.handle, int(seed) & (2**64 - 1), int(point), int(frame0), int(B),
                                                float(sigma2), int(max_iterations), _flags(early_stop, precision),
                                                _ptr(est), _ptr(ok), _ptr(its), None, _ptr(workspace), nb,
-                                               _native.current_stream_handle())
+                                               _native.current_stream_handle(g.device))
         _native.check(rc, "ldpc_decode_channel")
         return outputs
 
@@ -582,7 +582,8 @@ class ParallelDecoder:
         """Accumulate [bit errors, failures, iterations, frames] (all-zero codeword) into int64[4]."""
         est, ok, its, _ = outputs
         rc = _native.lib().ldpc_count_errors(self.tables.graph.handle, _ptr(est), _ptr(ok), _ptr(its),
-                                             int(ok.shape[0]), _ptr(counts_dev), _native.current_stream_handle())
+                                             int(ok.shape[0]), _ptr(counts_dev),
+                                             _native.current_stream_handle(self.tables.graph.device))
         _native.check(rc, "ldpc_count_errors")
 
     # engine.py:400-420
