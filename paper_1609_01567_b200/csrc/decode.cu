@@ -129,6 +129,8 @@ Workspace tile_view(const ldpc_graph *g, const Workspace &w, int32_t group0, int
 
 namespace {
 
+constexpr size_t kMaxGraphKeys = 256;  // distinct (pointers, sizes, flags, stream) keys cached per code
+
 // ---- per-kernel-class event timing ------------------------------------------
 struct Prof {
     ldpc_profile *out = nullptr;
@@ -439,37 +441,49 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
         auto *gg = const_cast<ldpc_graph *>(g);
         const ldpc_graph::GraphKey key{p_dev, B, max_iterations, flags, est_bits_dev, success_dev, iters_dev,
                                        syn_bits_dev, workspace_dev, stream};
-        ldpc_graph::GraphEntry *entry;
+        std::shared_ptr<ldpc_graph::GraphEntry> entry;
+        bool capture = false;
         {
             std::lock_guard<std::mutex> lock(gg->graphs_mu);
-            entry = &gg->graphs[key];
+            auto it = gg->graphs.find(key);
+            if (it == gg->graphs.end()) {
+                if (gg->graphs.size() >= kMaxGraphKeys)  // bounded: drop keys that never repeated
+                    for (auto e = gg->graphs.begin(); e != gg->graphs.end();)
+                        e = (e->second->exec == nullptr && !e->second->capturing) ? gg->graphs.erase(e) : std::next(e);
+                it = gg->graphs.emplace(key, std::make_shared<ldpc_graph::GraphEntry>()).first;
+            }
+            entry = it->second;
             entry->uses++;
+            if (entry->exec == nullptr && !entry->capturing && entry->uses >= 2) capture = entry->capturing = true;
         }
-        if (entry->exec == nullptr && entry->uses >= 2) {
+        if (capture) {
             cudaGraph_t graph = nullptr;
             const long long k0 = ldpc_kernel_launches();
-            LDPC_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-            int r = sequence(prof);
-            cudaError_t ce = cudaStreamEndCapture(s, &graph);
+            cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+            int r = LDPC_OK;
+            if (ce == cudaSuccess) {
+                r = sequence(prof);
+                ce = cudaStreamEndCapture(s, &graph);
+            }
             const long long kernels = ldpc_kernel_launches() - k0;
             count_launches(-kernels);  // captured, not executed
-            if (r != LDPC_OK || ce != cudaSuccess || graph == nullptr) {
-                if (graph) cudaGraphDestroy(graph);
+            cudaGraphExec_t exec = nullptr;
+            if (r == LDPC_OK && ce == cudaSuccess && graph != nullptr) ce = cudaGraphInstantiate(&exec, graph, 0);
+            if (graph) cudaGraphDestroy(graph);
+            {
+                std::lock_guard<std::mutex> lock(gg->graphs_mu);
+                entry->capturing = false;
+                if (exec) {
+                    entry->exec = exec;
+                    entry->kernels = kernels;
+                }
+            }
+            if (r != LDPC_OK) return r;
+            if (exec == nullptr) {
                 cudaGetLastError();
-                if (r != LDPC_OK) return r;
                 set_error("graph capture: %s", cudaGetErrorString(ce));
                 return LDPC_ECUDA;
             }
-            cudaGraphExec_t exec = nullptr;
-            ce = cudaGraphInstantiate(&exec, graph, 0);
-            cudaGraphDestroy(graph);
-            if (ce != cudaSuccess) {
-                set_error("graph instantiate: %s", cudaGetErrorString(ce));
-                return LDPC_ECUDA;
-            }
-            std::lock_guard<std::mutex> lock(gg->graphs_mu);
-            entry->exec = exec;
-            entry->kernels = kernels;
         }
         if (entry->exec != nullptr) {
             LDPC_CUDA_TRY(cudaGraphLaunch(entry->exec, s));

@@ -364,8 +364,7 @@ void free_graph(ldpc_graph *g) {
     if (!g) return;
     DeviceGuard dg(g->device);
     onchip_forget(g);
-    for (auto &kv : g->graphs)
-        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    g->graphs.clear();  // GraphEntry destructors release the executable graphs
     cudaFree(g->var_slot_ord);
     cudaFree(g->chk_slot_ord);
     cudaFree(g->chk_var_ord);
