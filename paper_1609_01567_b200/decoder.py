@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -131,15 +132,29 @@ def _tables_of(obj) -> CodeTables:
     if isinstance(obj, CodeTables):
         return obj
     if isinstance(obj, ParityCheckMatrix):
-        cache = _H_TABLES.get(id(obj))
-        if cache is None or cache[0] is not obj:
-            cache = (obj, CodeTables.from_matrix(obj))
-            _H_TABLES[id(obj)] = cache
-        return cache[1]
+        # device tables of a matrix passed where the reference takes H (syndrome, decode_awgn),
+        # kept while the matrix lives
+        tables = _H_TABLES.get(obj)
+        if tables is None:
+            tables = CodeTables.from_matrix(obj)
+            _H_TABLES[obj] = tables
+        return tables
     raise TypeError("expected CodeTables or ParityCheckMatrix")
 
 
-_H_TABLES: dict = {}
+class _IdentityKeyed(dict):
+    """id(matrix) -> tables, dropped when the matrix is collected."""
+
+    def get(self, obj, default=None):
+        return super().get(id(obj), default)
+
+    def __setitem__(self, obj, tables):
+        key = id(obj)
+        super().__setitem__(key, tables)
+        weakref.finalize(obj, self.pop, key, None)
+
+
+_H_TABLES = _IdentityKeyed()
 
 
 def _as_batch(a, width: int, what: str) -> tuple[np.ndarray, bool]:
