@@ -463,16 +463,28 @@ class ParallelDecoder:
                                                       np.empty((B, (m + 31) // 32), np.uint32), n, m)
         L = _native.lib()
         flags = _flags(early_stop, precision, schedule)
-        with self._lock:
+        if B > self.max_batch:
+            # several chunks: two in flight through the streaming slots, so the copy of chunk k+1
+            # overlaps the decode of chunk k (results identical to the per-chunk synchronous call)
+            pending = []
             for c0 in range(0, B, self.max_batch):
                 c1 = min(B, c0 + self.max_batch)
-                rc = L.ldpc_decoder_decode_host(
-                    self._h, P[c0:c1].ctypes.data, c1 - c0, int(max_iterations), flags,
-                    res.est_bits[c0:c1].ctypes.data, res.success[c0:c1].ctypes.data,
-                    res.iterations[c0:c1].ctypes.data, res.syn_bits[c0:c1].ctypes.data)
-                if rc == _native.LDPC_ECUDA or rc == _native.LDPC_ECLOSED:
-                    self._closed = True   # engine.py:389-392: poisoned after a device fault
-                _native.check(rc, "decode")
+                view = BatchResult(res.est_bits[c0:c1], res.success[c0:c1], res.iterations[c0:c1],
+                                   res.syn_bits[c0:c1], n, m)
+                pending.append(self.decode_priors_async(P[c0:c1], max_iterations, early_stop, out=view,
+                                                        precision=precision, schedule=schedule))
+                if len(pending) == 2:
+                    pending.pop(0).wait()
+            for job in pending:
+                job.wait()
+            return res
+        with self._lock:
+            rc = L.ldpc_decoder_decode_host(self._h, P.ctypes.data, B, int(max_iterations), flags,
+                                            res.est_bits.ctypes.data, res.success.ctypes.data,
+                                            res.iterations.ctypes.data, res.syn_bits.ctypes.data)
+            if rc == _native.LDPC_ECUDA or rc == _native.LDPC_ECLOSED:
+                self._closed = True   # engine.py:389-392: poisoned after a device fault
+            _native.check(rc, "decode")
         return res
 
     def decode_priors_async(self, P, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,

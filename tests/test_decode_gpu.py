@@ -265,3 +265,20 @@ def test_streaming_submit_wait_matches_sync(cuda):
             assert np.array_equal(streamed[0].syndromes(), z) and np.array_equal(streamed[0].success.astype(bool), ok)
         with pytest.raises(ValueError):
             dec.decode_priors_async(np.zeros((97, H.n)), 20)
+
+
+def test_batches_larger_than_max_batch_are_pipelined(cuda):
+    # B > max_batch: chunks of max_batch go two at a time through the streaming slots;
+    # results equal one whole-batch call and the oracle
+    from oracle import OracleTables
+
+    H, P = _frames("C1", 150, 1.5, seed=12)
+    T = CodeTables.from_matrix(H)
+    with ParallelDecoder(T, max_batch=64) as small, ParallelDecoder(T, max_batch=150) as big:
+        for early in (True, False):
+            a = small.decode_priors(P, 30, early_stop=early)
+            b = big.decode_priors(P, 30, early_stop=early)
+            assert np.array_equal(a.est_bits, b.est_bits) and np.array_equal(a.syn_bits, b.syn_bits)
+            assert np.array_equal(a.success, b.success) and np.array_equal(a.iterations, b.iterations)
+    est, ok, its, z = OracleTables.from_matrix(H).decode_batch(P, 30, fixed_iterations=True)
+    assert np.array_equal(a.estimates(), est) and np.array_equal(a.iterations, its)
