@@ -89,3 +89,16 @@ def test_unpack_bits_layout():
     words = np.array([[0b1011, 1 << 31]], dtype=np.uint32)
     bits = unpack_bits(words, 64)
     assert bits[0, :4].tolist() == [1, 1, 0, 1] and bits[0, 63] == 1 and bits.sum() == 4
+
+
+def test_plan_pages_mirrors_engine():
+    # engine.py:33-55: pages of group_size lanes, the last one partial; same errors
+    from paper_1609_01567_b200 import PagePlan, plan_pages
+
+    plan = plan_pages(10, 4)
+    assert plan == PagePlan(10, 4, (0, 4, 8))
+    assert plan.page_count == 3 and [plan.page_width(k) for k in range(3)] == [4, 4, 2]
+    assert plan_pages(7, 512).page_starts == (0,) and plan_pages(7, 1).page_count == 7
+    for bad in ((10, 0), (0, 4), (-1, 3)):
+        with pytest.raises(ValueError):
+            plan_pages(*bad)
