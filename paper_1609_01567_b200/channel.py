@@ -213,18 +213,27 @@ def gpu_decode_counts(decoder):
     return run
 
 
-def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int = 0,
-              batch: int = DEFAULT_BATCH, rate: float | None = None, decode_fn=None,
+def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int = 0, group_size: int = 512,
+              decoders_in_flight: int = 1, rate: float | None = None, *, batch: int = DEFAULT_BATCH, decode_fn=None,
               exact_channel: bool = False, device=None, channel: str = "host",
               precision: str = "fp64") -> list[BerPoint]:
     """channel.py:83-137 on the GPU, frames sharded over torch.distributed ranks.
 
+    The first eight parameters are the reference's, in its order; ``group_size`` and
+    ``decoders_in_flight`` are validated and otherwise unused (the GPU decodes ``batch``
+    frames per call instead of pages and decoders in flight).
     decode_fn(Y [b, n], sigma2, max_iterations, counts) must add
     [bit errors, failures, iterations, frames] of the batch into the int64[4]
     tensor ``counts``; the default decodes on this rank's GPU.
+    exact_channel=True draws the noise with the reference's scalar math (bit-identical
+    BerPoints); the default vectorised channel is statistically identical.
     channel="device" (f1) generates the noise and priors on the GPU as well
     (integer-exact RNG streams, device transcendentals: statistical parity).
     """
+    if group_size < 1:
+        raise ValueError("group_size must be at least 1")
+    if decoders_in_flight < 1:
+        raise ValueError("decoders_in_flight must be at least 1")
     if channel not in ("host", "device"):
         raise ValueError("channel must be 'host' or 'device'")
     if channel == "device":
