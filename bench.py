@@ -63,6 +63,15 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
+def synthetic_observations(H, B, ebno_db, seed):
+    """All-zero codeword, BPSK 0 -> -1, AWGN (channel.py:1-8): channel outputs y [B, n] and sigma^2."""
+    from paper_1609_01567_b200 import configs
+
+    s2 = configs.ebno_to_sigma2(ebno_db, configs.rate(H))
+    rng = np.random.default_rng(seed)
+    return -1.0 + np.sqrt(s2) * rng.standard_normal((B, H.n)), s2
+
+
 def synthetic_priors(H, B, ebno_db, seed):
     """All-zero codeword, BPSK 0 -> -1, AWGN (channel.py:1-8); priors by the reference's numpy expression."""
     from paper_1609_01567_b200 import configs, priors_awgn_batch
@@ -314,7 +323,7 @@ def run_ours(args):
     algo_bytes_step = sum(v["bytes"] for v in pd.values()) / args.steps
 
     # e2e through the public host API: pinned priors in, packed results out, every step
-    e2e = e2e_stream = None
+    e2e = e2e_stream = e2e_from_y = None
     if not args.no_e2e:
         from paper_1609_01567_b200.decoder import BatchResult
 
@@ -356,6 +365,25 @@ def run_ours(args):
             for q in pend:
                 q.wait()
 
+        # from channel observations: decode_batch(Y, sigma2), the reference's decode(y, sigma2) per frame
+        # batched -- priors by the reference's numpy expression on the host threads, then decode_priors
+        Y_host, s2_y = synthetic_observations(H, B, args.ebno, seed=2000 + rank)
+        Y_pin = torch.from_numpy(Y_host).pin_memory().numpy()
+        for _ in range(max(1, args.warmup)):
+            dec.decode_batch(Y_pin, s2_y, iters, early_stop=False)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            dec.decode_batch(Y_pin, s2_y, iters, early_stop=False)
+        el_y = time.perf_counter() - t0
+        ty = torch.tensor([el_y], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ty, op=dist.ReduceOp.MAX)
+        el_y = float(ty.item())
+        e2e_from_y = {"value": world * B * n * args.steps / el_y / 1e9, "unit": UNIT,
+                      "h2d_bytes_per_step": int(Y_host.nbytes), "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                      "ms_per_step": 1e3 * el_y / args.steps,
+                      "path": "ParallelDecoder.decode_batch(Y, sigma2): priors by the reference's numpy expression on "
+                              f"{min(32, os.cpu_count() or 1)} host threads inside the timed region, then decode_priors"}
         stream_steps(max(2, args.warmup))
         if world > 1:
             dist.barrier()
@@ -444,6 +472,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_stream": e2e_stream,
+            "e2e_from_y": e2e_from_y,
             "fast_fp32": fast,
             "other_configs": others,
             "gpu_launches": int(launches),

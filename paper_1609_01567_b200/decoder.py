@@ -71,7 +71,7 @@ def priors_awgn(y, sigma2: float) -> np.ndarray:
 _prior_pool = None
 
 
-def priors_awgn_batch(Y, sigma2, threads: int | None = None) -> np.ndarray:
+def priors_awgn_batch(Y, sigma2, threads: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
     """priors_awgn over a [B, n] batch, rows fanned out over host threads.
 
     Element-wise identical to calling priors_awgn per frame (numpy's exp does
@@ -85,7 +85,10 @@ def priors_awgn_batch(Y, sigma2, threads: int | None = None) -> np.ndarray:
     s2 = np.broadcast_to(np.asarray(sigma2, dtype=np.float64), (Y.shape[0],))
     if (s2 <= 0).any():
         raise ValueError("sigma2 must be positive")
-    out = np.empty_like(Y)
+    if out is None:
+        out = np.empty_like(Y)
+    elif out.shape != Y.shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous float64 array shaped like Y")
     nt = threads or min(32, os.cpu_count() or 1)
     if nt <= 1 or Y.shape[0] == 1:
         for b in range(Y.shape[0]):
@@ -441,8 +444,25 @@ class ParallelDecoder:
         Y = np.asarray(Y, dtype=np.float64)
         if Y.ndim != 2 or Y.shape[1] != self.tables.n:
             raise ValueError(f"expected frames of {self.tables.n} observations")
-        return self.decode_priors(priors_awgn_batch(Y, sigma2), max_iterations, early_stop, precision=precision,
-                                  schedule=schedule)
+        B, n, m = Y.shape[0], self.tables.n, self.tables.m
+        s2 = np.broadcast_to(np.asarray(sigma2, dtype=np.float64), (B,))
+        res = BatchResult(np.empty((B, (n + 31) // 32), np.uint32), np.empty(B, np.uint8), np.empty(B, np.int32),
+                          np.empty((B, (m + 31) // 32), np.uint32), n, m)
+        # priors go into a reused pinned buffer (no page faults, full-speed copies), max_batch frames at a time
+        buf = self._pinned_priors()
+        for c0 in range(0, B, self.max_batch):
+            c1 = min(B, c0 + self.max_batch)
+            P = priors_awgn_batch(Y[c0:c1], s2[c0:c1], out=buf[:c1 - c0])
+            self.decode_priors(P, max_iterations, early_stop, precision=precision, schedule=schedule,
+                               out=BatchResult(res.est_bits[c0:c1], res.success[c0:c1], res.iterations[c0:c1],
+                                               res.syn_bits[c0:c1], n, m))
+        return res
+
+    def _pinned_priors(self) -> np.ndarray:
+        if getattr(self, "_pinned", None) is None:
+            torch = _torch()
+            self._pinned = torch.empty((self.max_batch, self.tables.n), dtype=torch.float64).pin_memory().numpy()
+        return self._pinned
 
     def decode_priors(self, P, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
                       out: BatchResult | None = None, precision: str = "fp64", schedule: str = "auto") -> BatchResult:
