@@ -87,12 +87,18 @@ def _declare(L):
     L.ldpc_decode_channel.restype = ctypes.c_int
     L.ldpc_phase_f32.argtypes = [vp, ctypes.c_int, vp, vp, vp, i32, vp, sz, vp]
     L.ldpc_phase_f32.restype = ctypes.c_int
+    L.ldpc_comm_unique_id.argtypes = [vp]
+    L.ldpc_comm_create.argtypes = [i32, i32, vp, ctypes.POINTER(vp)]
+    L.ldpc_allreduce_counts_i64.argtypes = [vp, vp, i32, vp]
+    L.ldpc_comm_destroy.argtypes = [vp]
+    L.ldpc_comm_destroy.restype = None
     L.ldpc_selftest_division.argtypes = [ctypes.c_uint64, i64, P_i64]
     L.ldpc_selftest_division.restype = ctypes.c_int
     for name in ("ldpc_graph_create", "ldpc_graph_info", "ldpc_graph_get_tables", "ldpc_graph_get_var_groups",
                  "ldpc_graph_get_buckets", "ldpc_decode", "ldpc_count_errors", "ldpc_phase_to_check",
                  "ldpc_phase_to_variable", "ldpc_phase_estimate", "ldpc_phase_syndrome", "ldpc_decoder_create",
-                 "ldpc_decoder_decode_host", "ldpc_decoder_submit", "ldpc_decoder_wait"):
+                 "ldpc_decoder_decode_host", "ldpc_decoder_submit", "ldpc_decoder_wait", "ldpc_comm_unique_id",
+                 "ldpc_comm_create", "ldpc_allreduce_counts_i64"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

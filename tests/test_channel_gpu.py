@@ -53,3 +53,28 @@ def test_device_sweep_large_code_close_to_host_channel(cuda):
     b = ch.ber_sweep(H, [1.5], 256, max_iterations=30, seed=3, batch=128, exact_channel=True)[0]
     assert abs(a.failures - b.failures) <= 3
     assert abs(a.mean_iterations - b.mean_iterations) <= 0.2
+
+
+def test_c_abi_error_count_allreduce_single_rank(cuda):
+    # G6 through the C ABI (NCCL loaded on first use): a one-rank communicator sums in place
+    import ctypes
+
+    import torch
+
+    from paper_1609_01567_b200 import _native
+
+    L = _native.lib()
+    uid = (ctypes.c_uint8 * 128)()
+    _native.check(L.ldpc_comm_unique_id(uid), "ldpc_comm_unique_id")
+    comm = ctypes.c_void_p()
+    _native.check(L.ldpc_comm_create(1, 0, uid, ctypes.byref(comm)), "ldpc_comm_create")
+    try:
+        counts = torch.tensor([3054220, 66560, 665600, 66560], dtype=torch.int64, device="cuda")
+        _native.check(L.ldpc_allreduce_counts_i64(comm, ctypes.c_void_p(counts.data_ptr()), 4,
+                                                  _native.current_stream_handle()), "allreduce")
+        torch.cuda.synchronize()
+        assert counts.tolist() == [3054220, 66560, 665600, 66560]
+        with pytest.raises(ValueError):
+            _native.check(L.ldpc_comm_create(2, 2, uid, ctypes.byref(ctypes.c_void_p())), "bad rank")
+    finally:
+        L.ldpc_comm_destroy(comm)
