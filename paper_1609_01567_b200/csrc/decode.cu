@@ -292,7 +292,7 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
 }
 
 // done bits of padded codewords (>= B) are set from the start in early-stop mode
-int init_flags(const Workspace &w, bool early, cudaStream_t s) {
+int init_flags(const Workspace &w, bool early, cudaStream_t s, int32_t chat_rows = 0, bool wide_vars = false) {
     LDPC_CUDA_TRY(cudaMemsetAsync(w.unsat, 0, sizeof(uint32_t) * w.NW, s));
     LDPC_CUDA_TRY(cudaMemsetAsync(w.done, 0, sizeof(uint32_t) * w.NW, s));
     if (early) {
@@ -306,6 +306,11 @@ int init_flags(const Workspace &w, bool early, cudaStream_t s) {
         int rc = launch_fill_u32(w.done + first_pad_word, 0xffffffffu, (size_t)(w.NW - first_pad_word), s);
         if (rc) return rc;
     }
+    // Estimate words whose old bits are read back get a defined value first (compute-sanitizer
+    // initcheck): the bits of stopped codewords are kept (padding codewords are stopped from the
+    // start), and high-degree tiles narrower than a word update their bits with atomics.
+    if (chat_rows > 0 && ((early && w.B != w.Bp) || wide_vars))
+        LDPC_CUDA_TRY(cudaMemsetAsync(w.chat, 0, sizeof(uint32_t) * (size_t)chat_rows * w.NWs, s));
     return LDPC_OK;
 }
 
@@ -365,7 +370,7 @@ static int32_t tile_groups(const ldpc_graph *g, const Workspace &w, bool fast) {
 // The decode proper on a carved workspace whose P is filled.
 int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s, Prof &prof,
                bool fast = false) {
-    int rc = init_flags(w, early, s);
+    int rc = init_flags(w, early, s, g->n, g->max_dv > kMaxRegDegree);
     if (rc) return rc;
     if (fast) {
         rc = launch_priors_to_f32(w.P, prior32(g, w), (size_t)g->n * w.Bp, s);

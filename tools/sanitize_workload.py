@@ -1,0 +1,47 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): every kernel
+family on tiny inputs -- graph build, streaming decode (check register kernel, variable ring kernels,
+syndrome, done flags, layout), on-chip decode (1 CTA and a 2-CTA cluster), high-degree chains
+kernels, fp32 fast mode, the phase API, the host and streaming decoders, the device channel."""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+from paper_1609_01567_b200 import (CodeTables, ParallelDecoder, configs, estimate, generate_irregular_code,  # noqa: E402
+                                   priors_awgn_batch, syndrome, values_to_check, values_to_variable)
+
+
+def priors(H, B, ebno, seed):
+    s2 = configs.ebno_to_sigma2(ebno, configs.rate(H))
+    rng = np.random.default_rng(seed)
+    return priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((B, H.n)), s2)
+
+
+H1 = configs.code("C1")
+T1 = CodeTables.from_matrix(H1)
+P1 = priors(H1, 8, 1.5, 1)
+with ParallelDecoder(T1, max_batch=8) as dec:
+    for sched in ("stream", "onchip"):
+        for early in (True, False):
+            dec.decode_priors(P1, 5, early_stop=early, schedule=sched)
+    dec.decode_priors(P1, 5, precision="fp32", schedule="stream")
+    dec.decode_priors_async(P1, 3).wait()
+    import torch
+    dev = torch.device("cuda", 0)
+    dec.decode_channel(1, 0, 0, 8, 0.7, 3, workspace=dec.workspace(8), outputs=dec.alloc_outputs(8, dev))
+rng = np.random.default_rng(2)
+q = rng.uniform(size=(2, H1.total_edges))
+r = values_to_variable(q, T1)
+values_to_check(P1[:2], r, T1)
+c = estimate(P1[:2], r, T1)
+syndrome(c, T1)
+# 2-CTA cluster on chip
+H2 = generate_irregular_code({8: 400, 3: 1200, 2: 2400}, 2000, seed=3)
+with ParallelDecoder(CodeTables.from_matrix(H2), max_batch=2) as dec:
+    dec.decode_priors(priors(H2, 2, 1.5, 4), 3, schedule="onchip")
+# high-degree chains kernels (shared-memory staging)
+H4 = generate_irregular_code({200: 2, 3: 3000, 2: 3000}, 2000, seed=5, check_degrees={600: 2})
+with ParallelDecoder(CodeTables.from_matrix(H4), max_batch=2) as dec:
+    dec.decode_priors(priors(H4, 2, 1.5, 6), 2, early_stop=False)
+torch.cuda.synchronize()
+print("sanitize workload done")
