@@ -199,7 +199,7 @@ def _dist_info():
     return None, 0, 1
 
 
-def gpu_decode_counts(decoder):
+def gpu_decode_counts(decoder, early_stop: bool = True, precision: str = "fp64"):
     """decode_fn for ber_sweep: GPU decode of a batch, error counts accumulated on the device."""
     import torch
 
@@ -207,7 +207,8 @@ def gpu_decode_counts(decoder):
 
     def run(Y, sigma2, max_iterations, counts):
         P = torch.from_numpy(priors_awgn_batch(Y, sigma2)).to(counts.device)
-        outs = decoder.decode_device(P, max_iterations, early_stop=True, syndrome_out=False)
+        outs = decoder.decode_device(P, max_iterations, early_stop=early_stop, syndrome_out=False,
+                                     precision=precision)
         decoder.count_errors(outs, counts)
 
     return run
@@ -216,7 +217,7 @@ def gpu_decode_counts(decoder):
 def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int = 0, group_size: int = 512,
               decoders_in_flight: int = 1, rate: float | None = None, *, batch: int = DEFAULT_BATCH, decode_fn=None,
               exact_channel: bool = False, device=None, channel: str = "host",
-              precision: str = "fp64") -> list[BerPoint]:
+              precision: str = "fp64", early_stop: bool = True) -> list[BerPoint]:
     """channel.py:83-137 on the GPU, frames sharded over torch.distributed ranks.
 
     The first eight parameters are the reference's, in its order; ``group_size`` and
@@ -229,6 +230,8 @@ def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int =
     BerPoints); the default vectorised channel is statistically identical.
     channel="device" (f1) generates the noise and priors on the GPU as well
     (integer-exact RNG streams, device transcendentals: statistical parity).
+    precision="fp32" selects the fast mode; early_stop=False runs every frame for max_iterations
+    (the reference always stops early).
     """
     if group_size < 1:
         raise ValueError("group_size must be at least 1")
@@ -237,7 +240,7 @@ def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int =
     if channel not in ("host", "device"):
         raise ValueError("channel must be 'host' or 'device'")
     if channel == "device":
-        return _ber_sweep_device(H, ebno_points, frames, max_iterations, seed, batch, rate, precision)
+        return _ber_sweep_device(H, ebno_points, frames, max_iterations, seed, batch, rate, precision, early_stop)
     import torch
 
     if frames < 1:
@@ -252,7 +255,7 @@ def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int =
         from .tables import CodeTables
 
         decoder = ParallelDecoder(CodeTables.from_matrix(H), max_batch=batch)
-        decode_fn = gpu_decode_counts(decoder)
+        decode_fn = gpu_decode_counts(decoder, early_stop, precision)
         device = device or torch.device("cuda", torch.cuda.current_device())
     device = device or torch.device("cpu")
     lo, hi = shard_range(frames, rank, world)
@@ -278,7 +281,7 @@ def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int =
     return points
 
 
-def _ber_sweep_device(H, ebno_points, frames, max_iterations, seed, batch, rate, precision):
+def _ber_sweep_device(H, ebno_points, frames, max_iterations, seed, batch, rate, precision, early_stop=True):
     """f1 path: channel, priors, decode and the error fold all on this rank's GPU."""
     import torch
 
@@ -301,7 +304,8 @@ def _ber_sweep_device(H, ebno_points, frames, max_iterations, seed, batch, rate,
             for b0 in range(lo, hi, batch):
                 b = min(hi, b0 + batch) - b0
                 o = tuple(x[:b] for x in outs)
-                dec.decode_channel(seed, index, b0, b, sigma2, max_iterations, workspace=ws, outputs=o,
+                dec.decode_channel(seed, index, b0, b, sigma2, max_iterations, early_stop=early_stop, workspace=ws,
+                                   outputs=o,
                                    precision=precision)
                 dec.count_errors(o, counts)
             if dist is not None:

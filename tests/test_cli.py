@@ -89,3 +89,17 @@ def test_gallager_generator_matches_reference_golden():
         generate_gallager_code(10, 1, 2)
     with pytest.raises(ValueError):
         generate_gallager_code(10, 3, 7)
+
+
+@pytest.mark.gpu
+def test_ber_precision_and_fixed_iterations(tmp_path, cuda):
+    H = configs.code("C1")
+    code = tmp_path / "c1.alist"
+    code.write_text(serialize_alist(H))
+    for extra in (["--fixed-iters"], ["--precision", "fp32"], ["--channel", "device", "--fixed-iters"]):
+        csv = tmp_path / "ber.csv"
+        assert cli.main(["ber", "--code", str(code), "--ebno", "1.5", "--frames", "32", "--max-iter", "8",
+                         "--batch", "32", "--out", str(csv)] + extra) == cli.EXIT_OK
+        row = csv.read_text().splitlines()[1].split(",")
+        if "--fixed-iters" in extra:
+            assert float(row[5]) == 8.0   # mean_iterations: every frame ran the full budget
