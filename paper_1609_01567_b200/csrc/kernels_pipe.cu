@@ -273,19 +273,19 @@ __device__ __forceinline__ void load_prior(const NodeLaunch &a, int node, int ch
 }
 
 template <int D, int V, bool IS_VAR, bool FLAG, int MINB>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
-__global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int64_t ntasks) {
+__device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, int64_t first, int64_t W,
+                                          unsigned char *wsm) {
+    // one warp's persistent task loop: tasks first, first + W, ... of a side's bucket,
+    // its ring (ids + stages) at wsm
     constexpr int ROWS = ring_rows<D, IS_VAR>();
     constexpr bool PREG = IS_VAR && !prior_in_ring<D, IS_VAR>();  // prior via registers
     constexpr int ROW = 32 * V;
     constexpr bool FP = !IS_VAR && FLAG;
     using R = Ring<ROWS, V, MINB>;
     constexpr int S = R::S;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int *ids = reinterpret_cast<int *>(smem + (size_t)warp * R::kBytes);  // [S][kIdsStride]
-    double *rows = reinterpret_cast<double *>(smem + (size_t)warp * R::kBytes + R::kIdsBytes);  // [S][ROWS][ROW]
-    const int64_t W = (int64_t)gridDim.x * kWarpsPerBlock;
-    const int64_t first = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+    const int lane = threadIdx.x & 31;
+    int *ids = reinterpret_cast<int *>(wsm);                          // [S][kIdsStride]
+    double *rows = reinterpret_cast<double *>(wsm + R::kIdsBytes);    // [S][ROWS][ROW]
     if (first >= ntasks) return;
     const int ntask = (int)((ntasks - first + W - 1) / W);  // this warp's tasks: first, first + W, ...
 
@@ -363,6 +363,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int6
         __syncwarp();  // stage s is reused by the issue of the next iteration
     }
     cp_wait<0>();
+}
+
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
+__global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int64_t ntasks) {
+    using R = Ring<ring_rows<D, IS_VAR>(), V, MINB>;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5;
+    ring_loop<D, V, IS_VAR, FLAG, MINB>(a, ntasks, (int64_t)blockIdx.x * kWarpsPerBlock + warp,
+                                        (int64_t)gridDim.x * kWarpsPerBlock, smem + (size_t)warp * R::kBytes);
 }
 
 // Codewords per lane: V=1 (3 blocks/SM, more warps to hide the fp64 chains) for
