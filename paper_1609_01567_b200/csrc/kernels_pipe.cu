@@ -200,8 +200,10 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
                 out[v] = ddiv_fast(q1, __dadd_rn(q0, q1), ok);  // den == 0 -> !ok
                 all_ok = all_ok && ok;
             }
-            if (all_ok) st_v<V>(mb + row_off(ids[k]), out);
-            else slow |= 1u << k;
+            // stored unconditionally (no branch per output); the rare inexact ones are
+            // recomputed and overwritten below, later in this thread's program order
+            st_v<V>(mb + row_off(ids[k]), out);
+            if (!all_ok) slow |= 1u << k;
         }
 #pragma unroll
         for (int v = 0; v < V; v++) {
