@@ -366,7 +366,11 @@ def run_ours(args):
                 q.wait()
 
         # from channel observations: decode_batch(Y, sigma2), the reference's decode(y, sigma2) per frame
-        # batched -- priors by the reference's numpy expression on the host threads, then decode_priors
+        # batched -- priors formed on the device, bit-identical to the host's numpy (priors.cuh), when the
+        # probe says so; else by the reference's numpy expression on the host threads, then decode_priors
+        from paper_1609_01567_b200.decoder import device_priors_exact
+
+        dev_priors = device_priors_exact(dev.index or 0)
         Y_host, s2_y = synthetic_observations(H, B, args.ebno, seed=2000 + rank)
         Y_pin = torch.from_numpy(Y_host).pin_memory().numpy()
         for _ in range(max(1, args.warmup)):
@@ -382,8 +386,13 @@ def run_ours(args):
         e2e_from_y = {"value": world * B * n * args.steps / el_y / 1e9, "unit": UNIT,
                       "h2d_bytes_per_step": int(Y_host.nbytes), "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
                       "ms_per_step": 1e3 * el_y / args.steps,
-                      "path": "ParallelDecoder.decode_batch(Y, sigma2): priors by the reference's numpy expression on "
-                              f"{min(32, os.cpu_count() or 1)} host threads inside the timed region, then decode_priors"}
+                      "device_priors": dev_priors,
+                      "path": ("ParallelDecoder.decode_batch(Y, sigma2) (ldpc_decoder_decode_awgn_host): pinned H2D of "
+                               "the observations, priors formed in the layout kernel with numpy's exp algorithm "
+                               "(bit-identical; probe passed), decode, D2H" if dev_priors else
+                               "ParallelDecoder.decode_batch(Y, sigma2): priors by the reference's numpy expression "
+                               f"on {min(32, os.cpu_count() or 1)} host threads inside the timed region (this host's "
+                               "np.exp differs from the device prior), then decode_priors")}
         stream_steps(max(2, args.warmup))
         if world > 1:
             dist.barrier()

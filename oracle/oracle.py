@@ -6,10 +6,11 @@ package.  It is the checker the CUDA path is compared against, and the CPU
 baseline it is timed beside.
 
 The arithmetic lives in ldpc_oracle.c (a restatement of the reference's
-serial.py / tables.py, file:line cited there).  The one piece restated here
-in numpy is the prior, because the reference computes it with numpy's exp
-(serial.py:39-50) and the exact same numpy expression is the only way to get
-the same last-ulp values on the machine at hand.
+serial.py / tables.py, file:line cited there).  The prior is restated twice:
+priors_awgn() is the reference's own numpy expression (serial.py:39-50), the
+only way to get numpy's last-ulp values on the machine at hand; npexp.c
+restates the exp numpy runs on AVX512_SKX hosts (SVML exp8_ha) in C, the
+checker for the device prior kernel (priors_awgn_svml / npexp below).
 """
 
 from __future__ import annotations
@@ -42,8 +43,8 @@ _ERRORS = {
 
 def build(force: bool = False) -> pathlib.Path:
     """Compile the oracle (gcc, -ffp-contract=off) into oracle/build/."""
-    src = _HERE / "ldpc_oracle.c"
-    if force or not _LIB_PATH.exists() or _LIB_PATH.stat().st_mtime < src.stat().st_mtime:
+    srcs = [_HERE / "ldpc_oracle.c", _HERE / "npexp.c"]
+    if force or not _LIB_PATH.exists() or any(_LIB_PATH.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
     return _LIB_PATH
 
@@ -70,6 +71,10 @@ def lib():
         L.oracle_decode_batch.argtypes = [ctypes.c_void_p, _f64p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, _u8p, _u8p, _i32p, _u8p]
         L.oracle_decode_batch.restype = ctypes.c_int
+        L.oracle_npexp_array.argtypes = [_f64p, ctypes.c_long, _f64p]
+        L.oracle_npexp_array.restype = None
+        L.oracle_priors_awgn.argtypes = [_f64p, ctypes.c_long, ctypes.c_double, _f64p]
+        L.oracle_priors_awgn.restype = None
         _lib = L
     return _lib
 
@@ -85,6 +90,24 @@ def priors_awgn(y, sigma2: float) -> np.ndarray:
     y = np.asarray(y, dtype=np.float64)
     with np.errstate(over="ignore"):
         return 1.0 / (1.0 + np.exp(-2.0 * y / sigma2))
+
+
+def npexp(x) -> np.ndarray:
+    """npexp.c: numpy's AVX512_SKX float64 exp (SVML exp8_ha), restated in C."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    lib().oracle_npexp_array(_ptr(x, _f64p), x.size, _ptr(out, _f64p))
+    return out
+
+
+def priors_awgn_svml(y, sigma2: float) -> np.ndarray:
+    """serial.py:49-50 evaluated with npexp (one rounding per operation)."""
+    if sigma2 <= 0:
+        raise ValueError("sigma2 must be positive")
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.empty_like(y)
+    lib().oracle_priors_awgn(_ptr(y, _f64p), y.size, float(sigma2), _ptr(out, _f64p))
+    return out
 
 
 class OracleTables:

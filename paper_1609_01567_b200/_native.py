@@ -78,6 +78,11 @@ def _declare(L):
     L.ldpc_decoder_decode_host.argtypes = [vp, vp, i32, i32, u32, vp, vp, vp, vp]
     L.ldpc_decoder_submit.argtypes = [vp, vp, i32, i32, u32, vp, vp, vp, vp, P_i64]
     L.ldpc_decoder_wait.argtypes = [vp, i64]
+    L.ldpc_decode_awgn.argtypes = [vp, vp, vp, i32, i32, u32, vp, vp, vp, vp, vp, sz, vp, ctypes.POINTER(Profile)]
+    L.ldpc_priors_awgn.argtypes = [vp, vp, i32, i32, vp, vp]
+    L.ldpc_npexp.argtypes = [vp, i64, vp, vp]
+    L.ldpc_decoder_decode_awgn_host.argtypes = [vp, vp, vp, i32, i32, u32, vp, vp, vp, vp]
+    L.ldpc_decoder_submit_awgn.argtypes = [vp, vp, vp, i32, i32, u32, vp, vp, vp, vp, P_i64]
     L.ldpc_decoder_destroy.argtypes = [vp]
     L.ldpc_decoder_destroy.restype = None
     u64 = ctypes.c_uint64
@@ -98,7 +103,8 @@ def _declare(L):
                  "ldpc_graph_get_buckets", "ldpc_decode", "ldpc_count_errors", "ldpc_phase_to_check",
                  "ldpc_phase_to_variable", "ldpc_phase_estimate", "ldpc_phase_syndrome", "ldpc_decoder_create",
                  "ldpc_decoder_decode_host", "ldpc_decoder_submit", "ldpc_decoder_wait", "ldpc_comm_unique_id",
-                 "ldpc_comm_create", "ldpc_allreduce_counts_i64"):
+                 "ldpc_comm_create", "ldpc_allreduce_counts_i64", "ldpc_decode_awgn", "ldpc_priors_awgn",
+                 "ldpc_npexp", "ldpc_decoder_decode_awgn_host", "ldpc_decoder_submit_awgn"):
         getattr(L, name).restype = ctypes.c_int
     return L
 

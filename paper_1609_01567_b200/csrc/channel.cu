@@ -5,11 +5,12 @@
 // (rng.py:59-80, channel.py:112), maps 64-bit words to (0,1] (rng.py:44-50),
 // turns pairs of uniforms into normals with Box-Muller (channel.py:31-37) and
 // sends the all-zero codeword as y = -1 + sigma z (channel.py:47-67).  Here the
-// integer part (seeding, the stream, the uniforms) is bit-exact; Box-Muller and
-// the prior p = 1/(1+exp(-2y/s2)) (serial.py:39-50) use the device's fp64
-// log/sqrt/sincos/exp, which are not bit-identical to glibc / numpy, so parity
-// with the reference is statistical (tests/test_channel_gpu.py bounds the
-// difference of y and compares BER points).
+// integer part (seeding, the stream, the uniforms) is bit-exact; Box-Muller
+// uses the device's fp64 log/sqrt/sincos, which are not bit-identical to
+// glibc's, so y -- and parity with the reference -- is statistical
+// (tests/test_channel_gpu.py bounds the difference of y and compares BER
+// points).  The prior p = 1/(1+exp(-2y/s2)) of that y (serial.py:39-50) is
+// numpy's, bit for bit (priors.cuh).
 //
 // Parallelism: xorshift128+ is linear over GF(2)^128, so the state after s*L
 // draws is (M^L)^s times the seed state.  A host-built table of those 128x128
@@ -23,6 +24,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "priors.cuh"
 
 namespace ldpc {
 namespace {
@@ -108,8 +110,8 @@ __global__ void k_channel(uint64_t seed, uint64_t point, uint64_t frame0, int32_
             out[(size_t)f * n + j] = y0;
             if (j + 1 < n) out[(size_t)f * n + j + 1] = y1;
         } else {
-            out[cofs(n, j, f)] = 1.0 / (1.0 + exp(-2.0 * y0 / sigma2));
-            if (j + 1 < n) out[cofs(n, j + 1, f)] = 1.0 / (1.0 + exp(-2.0 * y1 / sigma2));
+            out[cofs(n, j, f)] = awgn_prior(y0, sigma2);
+            if (j + 1 < n) out[cofs(n, j + 1, f)] = awgn_prior(y1, sigma2);
         }
     }
 }

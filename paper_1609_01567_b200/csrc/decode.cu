@@ -395,10 +395,12 @@ extern "C" size_t ldpc_workspace_bytes(const ldpc_graph *g, int32_t B) {
     return workspace_bytes(g, B);
 }
 
-extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, int32_t max_iterations,
-                           uint32_t flags, uint32_t *est_bits_dev, uint8_t *success_dev, int32_t *iters_dev,
-                           uint32_t *syn_bits_dev, void *workspace_dev, size_t workspace_bytes_, void *stream,
-                           ldpc_profile *prof_host) {
+// p_dev: priors [B][n]; or, with sig2 != nullptr, observations y [B][n] whose priors are
+// formed inside the layout transpose (priors.cuh).
+static int decode_impl(const ldpc_graph *g, const double *p_dev, const double *sig2, int32_t B, int32_t max_iterations,
+                       uint32_t flags, uint32_t *est_bits_dev, uint8_t *success_dev, int32_t *iters_dev,
+                       uint32_t *syn_bits_dev, void *workspace_dev, size_t workspace_bytes_, void *stream,
+                       ldpc_profile *prof_host) {
     LDPC_ARG_CHECK(g != nullptr, "NULL graph");
     DeviceGuard dg(g->device);
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
@@ -418,7 +420,7 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
                    "the on-chip schedule needs a code whose messages fit 8 CTAs' shared memory (fp64)");
     if (cs > 0 && prof_host == nullptr) {
         LDPC_ARG_CHECK(B >= 1, "batch must be at least 1");
-        return launch_onchip(g, cs, p_dev, B, max_iterations, early, est_bits_dev, success_dev, iters_dev,
+        return launch_onchip(g, cs, p_dev, sig2, B, max_iterations, early, est_bits_dev, success_dev, iters_dev,
                              syn_bits_dev, s);
     }
     Workspace w;
@@ -426,7 +428,7 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
     if (rc) return rc;
     auto sequence = [&](Prof &prof) -> int {
         const int64_t n = g->n, m = g->m;
-        RUN(LDPC_KCLASS_LAYOUT, 16 * n * B, launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s));
+        RUN(LDPC_KCLASS_LAYOUT, 16 * n * B, launch_transpose_priors(p_dev, sig2, B, g->n, w.P, w.Bp, s));
         int r = run_decode(g, w, max_iterations, early, s, prof, fast);
         if (r) return r;
         RUN(LDPC_KCLASS_LAYOUT, (n / 8) * 2 * B, launch_pack_rows(w.chat, g->n, w.NW, B, est_bits_dev, s));
@@ -444,7 +446,7 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
         // (the first call runs eagerly and initialises every launcher), then
         // launched from the cache.
         auto *gg = const_cast<ldpc_graph *>(g);
-        const ldpc_graph::GraphKey key{p_dev, B, max_iterations, flags, est_bits_dev, success_dev, iters_dev,
+        const ldpc_graph::GraphKey key{p_dev, sig2, B, max_iterations, flags, est_bits_dev, success_dev, iters_dev,
                                        syn_bits_dev, workspace_dev, stream};
         std::shared_ptr<ldpc_graph::GraphEntry> entry;
         bool capture = false;
@@ -499,6 +501,23 @@ extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, 
     rc = sequence(prof);
     if (rc) return rc;
     return prof.flush();
+}
+
+extern "C" int ldpc_decode(const ldpc_graph *g, const double *p_dev, int32_t B, int32_t max_iterations,
+                           uint32_t flags, uint32_t *est_bits_dev, uint8_t *success_dev, int32_t *iters_dev,
+                           uint32_t *syn_bits_dev, void *workspace_dev, size_t workspace_bytes_, void *stream,
+                           ldpc_profile *prof_host) {
+    return decode_impl(g, p_dev, nullptr, B, max_iterations, flags, est_bits_dev, success_dev, iters_dev,
+                       syn_bits_dev, workspace_dev, workspace_bytes_, stream, prof_host);
+}
+
+extern "C" int ldpc_decode_awgn(const ldpc_graph *g, const double *y_dev, const double *sigma2_dev, int32_t B,
+                                int32_t max_iterations, uint32_t flags, uint32_t *est_bits_dev, uint8_t *success_dev,
+                                int32_t *iters_dev, uint32_t *syn_bits_dev, void *workspace_dev,
+                                size_t workspace_bytes_, void *stream, ldpc_profile *prof_host) {
+    LDPC_ARG_CHECK(sigma2_dev != nullptr, "NULL sigma2");
+    return decode_impl(g, y_dev, sigma2_dev, B, max_iterations, flags, est_bits_dev, success_dev, iters_dev,
+                       syn_bits_dev, workspace_dev, workspace_bytes_, stream, prof_host);
 }
 
 // f1: channel prologue on the device (noise + priors), then the same decode sequence
@@ -562,7 +581,7 @@ extern "C" int ldpc_phase_to_check(const ldpc_graph *g, const double *p_dev, con
     int rc = carve_workspace(g, B, ws, ws_bytes, &w);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    if ((rc = launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s))) return rc;
+    if ((rc = launch_transpose_priors(p_dev, nullptr, B, g->n, w.P, w.Bp, s))) return rc;
     if ((rc = launch_canon_to_slots(g, r_dev, B, w.msg, w.Bp, s))) return rc;
     if ((rc = var_phase(g, w, true, nullptr, s))) return rc;
     return launch_slots_to_canon(g, w.msg, w.Bp, q_dev, B, s);
@@ -576,7 +595,7 @@ extern "C" int ldpc_phase_estimate(const ldpc_graph *g, const double *p_dev, con
     int rc = carve_workspace(g, B, ws, ws_bytes, &w);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    if ((rc = launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s))) return rc;
+    if ((rc = launch_transpose_priors(p_dev, nullptr, B, g->n, w.P, w.Bp, s))) return rc;
     if ((rc = launch_canon_to_slots(g, r_dev, B, w.msg, w.Bp, s))) return rc;
     if ((rc = var_phase(g, w, false, nullptr, s))) return rc;
     return launch_bits_to_bytes(w.chat, g->n, w.NW, B, chat_dev, s);
@@ -609,7 +628,7 @@ extern "C" int ldpc_phase_f32(const ldpc_graph *g, int phase, const double *p_de
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     if (phase == 0) {
-        if ((rc = launch_transpose_priors(p_dev, B, g->n, w.P, w.Bp, s))) return rc;
+        if ((rc = launch_transpose_priors(p_dev, nullptr, B, g->n, w.P, w.Bp, s))) return rc;
         if ((rc = launch_priors_to_f32(w.P, prior32(g, w), (size_t)g->n * w.Bp, s))) return rc;
     }
     if ((rc = launch_canon_to_slots_f32(g, in_dev, B, msg32(g, w), w.Bp, s))) return rc;
@@ -651,7 +670,8 @@ struct ldpc_decoder {
     void *ws[kLanes] = {};             // ... in workspace ws[i % lanes]
     int lanes = 1;
     size_t ws_bytes = 0;
-    double *p = nullptr;      // [max_batch][n]
+    double *p = nullptr;      // [max_batch][n] priors or observations
+    double *s2 = nullptr;     // [max_batch] noise variances (observation input)
     uint32_t *est = nullptr;  // [max_batch][RWn]
     uint32_t *syn = nullptr;  // [max_batch][RWm]
     uint8_t *succ = nullptr;  // [max_batch]
@@ -659,7 +679,7 @@ struct ldpc_decoder {
     cudaEvent_t in_ready[kMaxChunks] = {}, decoded[kMaxChunks] = {};
     // streaming slots (ldpc_decoder_submit / wait), allocated on first use
     struct Slot {
-        double *p = nullptr;
+        double *p = nullptr, *s2 = nullptr;
         uint32_t *est = nullptr, *syn = nullptr;
         uint8_t *succ = nullptr;
         int32_t *its = nullptr;
@@ -682,6 +702,7 @@ static void decoder_free(ldpc_decoder *d) {
     cudaFree(d->ws_full);
     for (auto &sl : d->slots) {
         cudaFree(sl.p);
+        cudaFree(sl.s2);
         cudaFree(sl.est);
         cudaFree(sl.syn);
         cudaFree(sl.succ);
@@ -690,6 +711,7 @@ static void decoder_free(ldpc_decoder *d) {
             if (e) cudaEventDestroy(e);
     }
     cudaFree(d->p);
+    cudaFree(d->s2);
     cudaFree(d->est);
     cudaFree(d->syn);
     cudaFree(d->succ);
@@ -752,6 +774,7 @@ extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32
         if (e == cudaSuccess) e = cudaMalloc(&d->ws[l], d->ws_bytes);
     }
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->p, sizeof(double) * (size_t)g->n * MB);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->s2, sizeof(double) * MB);
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->est, sizeof(uint32_t) * RWn * MB);
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->syn, sizeof(uint32_t) * RWm * MB);
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->succ, MB);
@@ -768,9 +791,9 @@ extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32
     return LDPC_OK;
 }
 
-extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, int32_t B, int32_t max_iterations,
-                                        uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
-                                        int32_t *iters_host, uint32_t *syn_bits_host) {
+static int decoder_run(ldpc_decoder *d, const double *p_host, const double *s2_host, int32_t B,
+                       int32_t max_iterations, uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
+                       int32_t *iters_host, uint32_t *syn_bits_host) {
     if (d == nullptr) {
         set_error("decoder is closed");
         return LDPC_ECLOSED;
@@ -796,9 +819,11 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
         }
     };
     // 1. every H2D copy, back to back on the copy stream
+    if (s2_host)
+        cuda(cudaMemcpyAsync(d->s2, s2_host, sizeof(double) * B, cudaMemcpyHostToDevice, d->s_in), "H2D sigma2");
     for (size_t i = 0, c0 = 0; i < plan.size(); c0 += plan[i], i++) {
         cuda(cudaMemcpyAsync(d->p + c0 * n, p_host + c0 * n, sizeof(double) * n * plan[i], cudaMemcpyHostToDevice,
-                             d->s_in), "H2D priors");
+                             d->s_in), s2_host ? "H2D observations" : "H2D priors");
         cuda(cudaEventRecord(d->in_ready[i], d->s_in), "record");
     }
     // 2. decodes in order, each results copy right behind its decode
@@ -807,8 +832,9 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
         const int l = (int)(i % d->lanes);
         cuda(cudaStreamWaitEvent(d->s_comp[l], d->in_ready[i], 0), "wait input");
         if (e != cudaSuccess) break;
-        rc = ldpc_decode(g, d->p + c0 * n, b, max_iterations, flags, d->est + c0 * RWn, d->succ + c0, d->its + c0,
-                         syn_bits_host ? d->syn + c0 * RWm : nullptr, d->ws[l], d->ws_bytes, d->s_comp[l], nullptr);
+        rc = decode_impl(g, d->p + c0 * n, s2_host ? d->s2 + c0 : nullptr, b, max_iterations, flags,
+                         d->est + c0 * RWn, d->succ + c0, d->its + c0, syn_bits_host ? d->syn + c0 * RWm : nullptr,
+                         d->ws[l], d->ws_bytes, d->s_comp[l], nullptr);
         if (rc) break;
         cuda(cudaEventRecord(d->decoded[i], d->s_comp[l]), "record");
         cuda(cudaStreamWaitEvent(d->s_out, d->decoded[i], 0), "wait decode");
@@ -826,6 +852,22 @@ extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, i
     if (rc == LDPC_OK && e != cudaSuccess) rc = LDPC_ECUDA;
     if (rc == LDPC_ECUDA) d->poisoned = true;  // mirrors engine.py:389-392: refuse further use
     return rc;
+}
+
+extern "C" int ldpc_decoder_decode_host(ldpc_decoder *d, const double *p_host, int32_t B, int32_t max_iterations,
+                                        uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
+                                        int32_t *iters_host, uint32_t *syn_bits_host) {
+    return decoder_run(d, p_host, nullptr, B, max_iterations, flags, est_bits_host, success_host, iters_host,
+                       syn_bits_host);
+}
+
+extern "C" int ldpc_decoder_decode_awgn_host(ldpc_decoder *d, const double *y_host, const double *sigma2_host,
+                                             int32_t B, int32_t max_iterations, uint32_t flags,
+                                             uint32_t *est_bits_host, uint8_t *success_host, int32_t *iters_host,
+                                             uint32_t *syn_bits_host) {
+    LDPC_ARG_CHECK(sigma2_host != nullptr, "NULL sigma2");
+    return decoder_run(d, y_host, sigma2_host, B, max_iterations, flags, est_bits_host, success_host, iters_host,
+                       syn_bits_host);
 }
 
 // ---- streaming: submit / wait ---------------------------------------------------
@@ -850,6 +892,7 @@ static int slots_alloc(ldpc_decoder *d) {
     e = cudaMalloc(&d->ws_full, d->ws_full_bytes);
     for (auto &sl : d->slots) {
         if (e == cudaSuccess) e = cudaMalloc((void **)&sl.p, sizeof(double) * (size_t)g->n * MB);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&sl.s2, sizeof(double) * MB);
         if (e == cudaSuccess) e = cudaMalloc((void **)&sl.est, sizeof(uint32_t) * RWn * MB);
         if (e == cudaSuccess) e = cudaMalloc((void **)&sl.syn, sizeof(uint32_t) * RWm * MB);
         if (e == cudaSuccess) e = cudaMalloc((void **)&sl.succ, MB);
@@ -865,9 +908,9 @@ static int slots_alloc(ldpc_decoder *d) {
     return LDPC_OK;
 }
 
-extern "C" int ldpc_decoder_submit(ldpc_decoder *d, const double *p_host, int32_t B, int32_t max_iterations,
-                                   uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
-                                   int32_t *iters_host, uint32_t *syn_bits_host, int64_t *ticket) {
+static int decoder_submit(ldpc_decoder *d, const double *p_host, const double *s2_host, int32_t B,
+                          int32_t max_iterations, uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
+                          int32_t *iters_host, uint32_t *syn_bits_host, int64_t *ticket) {
     if (d == nullptr) {
         set_error("decoder is closed");
         return LDPC_ECLOSED;
@@ -896,11 +939,12 @@ extern "C" int ldpc_decoder_submit(ldpc_decoder *d, const double *p_host, int32_
             set_error("%s: %s", what, cudaGetErrorString(x));
         }
     };
-    cuda(cudaMemcpyAsync(sl.p, p_host, sizeof(double) * n * B, cudaMemcpyHostToDevice, d->s_in), "H2D priors");
+    if (s2_host) cuda(cudaMemcpyAsync(sl.s2, s2_host, sizeof(double) * B, cudaMemcpyHostToDevice, d->s_in), "H2D sigma2");
+    cuda(cudaMemcpyAsync(sl.p, p_host, sizeof(double) * n * B, cudaMemcpyHostToDevice, d->s_in), "H2D input");
     cuda(cudaEventRecord(sl.in_done, d->s_in), "record");
     cuda(cudaStreamWaitEvent(sc, sl.in_done, 0), "wait input");
     if (e == cudaSuccess)
-        rc = ldpc_decode(g, sl.p, B, max_iterations, flags, sl.est, sl.succ, sl.its,
+        rc = decode_impl(g, sl.p, s2_host ? sl.s2 : nullptr, B, max_iterations, flags, sl.est, sl.succ, sl.its,
                          syn_bits_host ? sl.syn : nullptr, d->ws_full, d->ws_full_bytes, sc, nullptr);
     if (rc == LDPC_OK && e == cudaSuccess) {
         cuda(cudaEventRecord(sl.dec_done, sc), "record");
@@ -925,6 +969,22 @@ extern "C" int ldpc_decoder_submit(ldpc_decoder *d, const double *p_host, int32_
     d->next_ticket = k + 1;
     *ticket = k;
     return LDPC_OK;
+}
+
+extern "C" int ldpc_decoder_submit(ldpc_decoder *d, const double *p_host, int32_t B, int32_t max_iterations,
+                                   uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
+                                   int32_t *iters_host, uint32_t *syn_bits_host, int64_t *ticket) {
+    return decoder_submit(d, p_host, nullptr, B, max_iterations, flags, est_bits_host, success_host, iters_host,
+                          syn_bits_host, ticket);
+}
+
+extern "C" int ldpc_decoder_submit_awgn(ldpc_decoder *d, const double *y_host, const double *sigma2_host, int32_t B,
+                                        int32_t max_iterations, uint32_t flags, uint32_t *est_bits_host,
+                                        uint8_t *success_host, int32_t *iters_host, uint32_t *syn_bits_host,
+                                        int64_t *ticket) {
+    LDPC_ARG_CHECK(sigma2_host != nullptr, "NULL sigma2");
+    return decoder_submit(d, y_host, sigma2_host, B, max_iterations, flags, est_bits_host, success_host, iters_host,
+                          syn_bits_host, ticket);
 }
 
 extern "C" int ldpc_decoder_wait(ldpc_decoder *d, int64_t ticket) {

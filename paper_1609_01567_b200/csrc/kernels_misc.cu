@@ -8,6 +8,7 @@
 // OR-reduction of z over checks: per thread in registers, per block in shared
 // memory, then one atomicOr per word per block.
 #include "common.cuh"
+#include "priors.cuh"
 
 namespace ldpc {
 namespace {
@@ -20,13 +21,21 @@ unsigned blocks_for(int64_t work, int threads, int64_t cap = 148 * 64) {
 }
 
 // P_in [B][n] -> P [Bp/64][n][64] (chunk-major); padded codewords get p = 0.5 (no information).
-__global__ void k_transpose_priors(const double *__restrict__ in, int32_t B, int32_t n, double *__restrict__ P,
-                                   int32_t Bp) {
+// AWGN: the input is observations y and the prior 1/(1+exp(-2y/sigma2[c])) is formed on the way
+// (priors.cuh, bit-identical to the reference's numpy expression).
+template <bool AWGN>
+__global__ void k_transpose_priors(const double *__restrict__ in, const double *__restrict__ sig2, int32_t B,
+                                   int32_t n, double *__restrict__ P, int32_t Bp) {
     __shared__ double tile[32][33];
     const int j0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {
         const int c = c0 + y, j = j0 + threadIdx.x;
-        tile[y][threadIdx.x] = (c < B && j < n) ? __ldcs(in + (size_t)c * n + j) : 0.5;
+        double v = 0.5;
+        if (c < B && j < n) {
+            v = __ldcs(in + (size_t)c * n + j);
+            if (AWGN) v = awgn_prior(v, __ldg(sig2 + c));
+        }
+        tile[y][threadIdx.x] = v;
     }
     __syncthreads();
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {
@@ -201,9 +210,13 @@ __global__ void k_fill_u32(uint32_t *dst, uint32_t value, size_t count) {
 
 }  // namespace
 
-int launch_transpose_priors(const double *p_in, int32_t B, int32_t n, double *P, int32_t Bp, cudaStream_t s) {
+int launch_transpose_priors(const double *p_in, const double *sig2, int32_t B, int32_t n, double *P, int32_t Bp,
+                            cudaStream_t s) {
     dim3 grid((n + 31) / 32, (Bp + 31) / 32);
-    k_transpose_priors<<<grid, dim3(32, 8), 0, s>>>(p_in, B, n, P, Bp);
+    if (sig2)
+        k_transpose_priors<true><<<grid, dim3(32, 8), 0, s>>>(p_in, sig2, B, n, P, Bp);
+    else
+        k_transpose_priors<false><<<grid, dim3(32, 8), 0, s>>>(p_in, nullptr, B, n, P, Bp);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }

@@ -37,6 +37,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "priors.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -51,7 +52,8 @@ struct OnchipArgs {
     int32_t sb[kOnchipMaxCS + 1];  // slot boundaries per rank
     int32_t cb[kOnchipMaxCS + 1];  // check-id boundaries per rank
     int32_t vb[kOnchipMaxCS + 1];  // var_order position boundaries per rank
-    const double *P;               // [B][n] priors (host layout)
+    const double *P;               // [B][n] priors (host layout), or observations y when sig2 != nullptr
+    const double *sig2;            // [B] noise variances: priors formed on chip (priors.cuh)
     const int32_t *var_off, *var_pos, *var_order, *inv_pos;  // canonical var CSR; slot of edge; order; position of var
     const int32_t *chk_off, *chk_var, *chk_list;              // check CSR over slots; var of slot; checks per rank by degree
     uint32_t *est;      // [B][RWn]
@@ -309,7 +311,13 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const __grid_constant
     for (int cw = cid; cw < a.B; cw += nclusters) {
         // priors of this rank's variables (serial.py:58: q = p[v] feeds the pre-pass)
         const double *Pc = a.P + (size_t)cw * a.n;
-        for (int i = threadIdx.x; i < nvars; i += blockDim.x) pl[i] = __ldg(Pc + __ldg(a.var_order + v0 + i));
+        if (a.sig2 == nullptr) {
+            for (int i = threadIdx.x; i < nvars; i += blockDim.x) pl[i] = __ldg(Pc + __ldg(a.var_order + v0 + i));
+        } else {
+            const double s2 = __ldg(a.sig2 + cw);
+            for (int i = threadIdx.x; i < nvars; i += blockDim.x)
+                pl[i] = awgn_prior(__ldg(Pc + __ldg(a.var_order + v0 + i)), s2);
+        }
         if (threadIdx.x < 2) flag[threadIdx.x] = 0;
         if (rank == 0) {
             for (int i = threadIdx.x; i < a.RWn; i += blockDim.x) erow[i] = 0u;
@@ -482,8 +490,8 @@ bool onchip_auto(const ldpc_graph *g, int32_t B) {
     return B <= 2 * res;
 }
 
-int launch_onchip(const ldpc_graph *g, int CS, const double *p_dev, int32_t B, int32_t max_iter, bool early,
-                  uint32_t *est, uint8_t *succ, int32_t *iters, uint32_t *syn, cudaStream_t s) {
+int launch_onchip(const ldpc_graph *g, int CS, const double *p_dev, const double *sig2, int32_t B, int32_t max_iter,
+                  bool early, uint32_t *est, uint8_t *succ, int32_t *iters, uint32_t *syn, cudaStream_t s) {
     Plan *pl;
     {
         std::lock_guard<std::mutex> lock(g_plan_mu);
@@ -512,6 +520,7 @@ int launch_onchip(const ldpc_graph *g, int CS, const double *p_dev, int32_t B, i
         a.vb[r] = pl->vb[r];
     }
     a.P = p_dev;
+    a.sig2 = sig2;
     a.var_off = g->var_off;
     a.var_pos = g->var_pos;
     a.var_order = g->var_order;

@@ -113,6 +113,54 @@ def initialize(y, sigma2: float, tables: CodeTables) -> MessageState:
     return MessageState(p, p[tables.variable.v], np.full(tables.total_edges, 0.5))
 
 
+# ---- device priors (observation input) -------------------------------------------
+
+_exact = {}
+_exact_mu = threading.Lock()
+
+
+def _exp_probe_inputs() -> np.ndarray:
+    """Fixed inputs on which candidate float64 exp implementations disagree: ~5% of
+    random arguments separate numpy's SVML exp from glibc's, so 2^17 of them (plus
+    both special-case regions and the rare path's bounds) leave no doubt."""
+    rng = np.random.default_rng(160901567)
+    edges = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-300, -1e-300, 2.0 ** -54, -(2.0 ** -54),
+                      709.78, 709.79, 707.70327135170, 707.70327135171, -707.70327135171, -708.39641853226,
+                      -708.39641853227, -745.13321910194, -745.13321910195, -740.0, -720.0])
+    return np.concatenate([rng.uniform(-40.0, 40.0, 1 << 17), rng.uniform(-746.0, 710.0, 1 << 14),
+                           rng.uniform(-746.0, -700.0, 1 << 12), rng.uniform(700.0, 710.0, 1 << 12),
+                           rng.normal(0.0, 1e-9, 1 << 10), edges])
+
+
+def device_priors_exact(device: int = 0) -> bool:
+    """Whether the device prior (csrc/priors.cuh) reproduces this host's np.exp bit for bit.
+
+    The reference forms priors with numpy (serial.py:49-50), whose float64 exp is
+    machine dependent; the device runs the algorithm numpy uses on AVX512_SKX hosts.
+    Checked once per process and device on _exp_probe_inputs(); when it fails the
+    decoder forms priors on the host with numpy instead, so results stay identical
+    to the reference either way.  LDPC_DEVICE_PRIORS=0 forces host priors.
+    """
+    if os.environ.get("LDPC_DEVICE_PRIORS", "") == "0":
+        return False
+    with _exact_mu:
+        if device in _exact:
+            return _exact[device]
+        torch = _torch()
+        x = _exp_probe_inputs()
+        with np.errstate(all="ignore"):
+            want = np.exp(x)
+        xd = torch.from_numpy(x).to(f"cuda:{device}")
+        out = torch.empty_like(xd)
+        with torch.cuda.device(device):
+            _native.check(_native.lib().ldpc_npexp(_ptr(xd), x.size, _ptr(out), _native.current_stream_handle(device)),
+                          "ldpc_npexp")
+        got = out.cpu().numpy()
+        same = (got.view(np.uint64) == want.view(np.uint64)) | (np.isnan(got) & np.isnan(want))
+        _exact[device] = bool(same.all())
+        return _exact[device]
+
+
 # ---- device plumbing ----------------------------------------------------------
 
 def _torch():
@@ -431,6 +479,14 @@ class ParallelDecoder:
             raise RuntimeError("decoder is closed")
         if max_iterations < 0:
             raise ValueError("max_iterations must be non-negative")
+        if device_priors_exact(self.tables.graph.device):
+            if sigma2 <= 0:
+                raise ValueError("sigma2 must be positive")
+            y = np.ascontiguousarray(y, dtype=np.float64)
+            if y.ndim != 1 or len(y) != self.tables.n:
+                raise ValueError(f"expected {self.tables.n} observations, got {len(y)}")
+            return self._run(y.reshape(1, -1), np.full(1, float(sigma2)), max_iterations, True, None, "fp64",
+                             "auto")[0]
         p = priors_awgn(y, sigma2)
         if p.ndim != 1 or len(p) != self.tables.n:
             raise ValueError(f"expected {self.tables.n} observations, got {len(p)}")
@@ -446,6 +502,13 @@ class ParallelDecoder:
             raise ValueError(f"expected frames of {self.tables.n} observations")
         B, n, m = Y.shape[0], self.tables.n, self.tables.m
         s2 = np.broadcast_to(np.asarray(sigma2, dtype=np.float64), (B,))
+        if device_priors_exact(self.tables.graph.device):
+            # observations go to the device as they are; the priors are formed there (priors.cuh),
+            # bit-identical to numpy's.  Pinned Y (torch pin_memory) copies at full speed.
+            if (s2 <= 0).any():
+                raise ValueError("sigma2 must be positive")
+            return self._run(np.ascontiguousarray(Y), np.ascontiguousarray(s2), max_iterations, early_stop, None,
+                             precision, schedule)
         res = BatchResult(np.empty((B, (n + 31) // 32), np.uint32), np.empty(B, np.uint8), np.empty(B, np.int32),
                           np.empty((B, (m + 31) // 32), np.uint32), n, m)
         # priors go into a reused pinned buffer (no page faults, full-speed copies), max_batch frames at a time
@@ -476,6 +539,10 @@ class ParallelDecoder:
         P = np.ascontiguousarray(P, dtype=np.float64)
         if P.ndim != 2 or P.shape[1] != self.tables.n:
             raise ValueError(f"expected priors of shape [B, {self.tables.n}]")
+        return self._run(P, None, max_iterations, early_stop, out, precision, schedule)
+
+    def _run(self, P, s2, max_iterations, early_stop, out, precision, schedule) -> BatchResult:
+        """Host [B, n] priors (s2 None) or observations with per-frame sigma2 [B] -> BatchResult."""
         B = P.shape[0]
         n, m = self.tables.n, self.tables.m
         res = out if out is not None else BatchResult(np.empty((B, (n + 31) // 32), np.uint32),
@@ -491,17 +558,21 @@ class ParallelDecoder:
                 c1 = min(B, c0 + self.max_batch)
                 view = BatchResult(res.est_bits[c0:c1], res.success[c0:c1], res.iterations[c0:c1],
                                    res.syn_bits[c0:c1], n, m)
-                pending.append(self.decode_priors_async(P[c0:c1], max_iterations, early_stop, out=view,
-                                                        precision=precision, schedule=schedule))
+                pending.append(self._submit(P[c0:c1], None if s2 is None else s2[c0:c1], max_iterations,
+                                            early_stop, view, precision, schedule))
                 if len(pending) == 2:
                     pending.pop(0).wait()
             for job in pending:
                 job.wait()
             return res
         with self._lock:
-            rc = L.ldpc_decoder_decode_host(self._h, P.ctypes.data, B, int(max_iterations), flags,
-                                            res.est_bits.ctypes.data, res.success.ctypes.data,
-                                            res.iterations.ctypes.data, res.syn_bits.ctypes.data)
+            outs = (res.est_bits.ctypes.data, res.success.ctypes.data, res.iterations.ctypes.data,
+                    res.syn_bits.ctypes.data)
+            if s2 is None:
+                rc = L.ldpc_decoder_decode_host(self._h, P.ctypes.data, B, int(max_iterations), flags, *outs)
+            else:
+                rc = L.ldpc_decoder_decode_awgn_host(self._h, P.ctypes.data, s2.ctypes.data, B, int(max_iterations),
+                                                     flags, *outs)
             if rc == _native.LDPC_ECUDA or rc == _native.LDPC_ECLOSED:
                 self._closed = True   # engine.py:389-392: poisoned after a device fault
             _native.check(rc, "decode")
@@ -522,6 +593,28 @@ class ParallelDecoder:
         P = np.ascontiguousarray(P, dtype=np.float64)
         if P.ndim != 2 or P.shape[1] != self.tables.n:
             raise ValueError(f"expected priors of shape [B, {self.tables.n}]")
+        return self._submit(P, None, max_iterations, early_stop, out, precision, schedule)
+
+    def decode_batch_async(self, Y, sigma2, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
+                           out: BatchResult | None = None, precision: str = "fp64",
+                           schedule: str = "auto") -> "PendingDecode":
+        """Streaming variant of decode_batch: observations [B, n] (B <= max_batch, pinned for
+        asynchronous copies) in, priors formed on the device.  Needs device_priors_exact()."""
+        if self._closed:
+            raise RuntimeError("decoder is closed")
+        if not device_priors_exact(self.tables.graph.device):
+            raise RuntimeError("this host's np.exp differs from the device prior; use decode_priors_async")
+        if max_iterations < 0:
+            raise ValueError("max_iterations must be non-negative")
+        Y = np.ascontiguousarray(Y, dtype=np.float64)
+        if Y.ndim != 2 or Y.shape[1] != self.tables.n:
+            raise ValueError(f"expected frames of {self.tables.n} observations")
+        s2 = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma2, dtype=np.float64), (Y.shape[0],)))
+        if (s2 <= 0).any():
+            raise ValueError("sigma2 must be positive")
+        return self._submit(Y, s2, max_iterations, early_stop, out, precision, schedule)
+
+    def _submit(self, P, s2, max_iterations, early_stop, out, precision, schedule) -> "PendingDecode":
         B = P.shape[0]
         if not 1 <= B <= self.max_batch:
             raise ValueError(f"batch {B} outside 1..{self.max_batch}")
@@ -530,15 +623,20 @@ class ParallelDecoder:
                                                       np.empty(B, np.uint8), np.empty(B, np.int32),
                                                       np.empty((B, (m + 31) // 32), np.uint32), n, m)
         ticket = ctypes.c_int64(-1)
-        with self._lock:
-            rc = _native.lib().ldpc_decoder_submit(
-                self._h, P.ctypes.data, B, int(max_iterations), _flags(early_stop, precision, schedule),
-                res.est_bits.ctypes.data, res.success.ctypes.data, res.iterations.ctypes.data,
+        L = _native.lib()
+        flags = _flags(early_stop, precision, schedule)
+        outs = (res.est_bits.ctypes.data, res.success.ctypes.data, res.iterations.ctypes.data,
                 res.syn_bits.ctypes.data, ctypes.byref(ticket))
+        with self._lock:
+            if s2 is None:
+                rc = L.ldpc_decoder_submit(self._h, P.ctypes.data, B, int(max_iterations), flags, *outs)
+            else:
+                rc = L.ldpc_decoder_submit_awgn(self._h, P.ctypes.data, s2.ctypes.data, B, int(max_iterations),
+                                                flags, *outs)
             if rc == _native.LDPC_ECUDA or rc == _native.LDPC_ECLOSED:
                 self._closed = True
             _native.check(rc, "decode")
-        return PendingDecode(self, ticket.value, P, res)
+        return PendingDecode(self, ticket.value, (P, s2), res)
 
     def decode_stream(self, batches, max_iterations: int = DEFAULT_MAX_ITERATIONS, early_stop: bool = True,
                       precision: str = "fp64"):
@@ -588,6 +686,34 @@ class ParallelDecoder:
                                        _native.current_stream_handle(g.device),
                                        ctypes.byref(profile) if profile is not None else None)
         _native.check(rc, "ldpc_decode")
+        return outputs
+
+    def decode_device_awgn(self, Y_dev, sigma2_dev, max_iterations: int, early_stop: bool = True, workspace=None,
+                           outputs=None, syndrome_out: bool = True, precision: str = "fp64",
+                           schedule: str = "auto"):
+        """Device observations [B, n] fp64 + sigma2 [B] fp64 -> device outputs; the priors are
+        formed on the device (priors.cuh; bit-identical to numpy's on AVX512_SKX hosts)."""
+        if self._closed:
+            raise RuntimeError("decoder is closed")
+        torch = _torch()
+        g = self.tables.graph
+        B = int(Y_dev.shape[0])
+        if Y_dev.dtype != torch.float64 or Y_dev.dim() != 2 or Y_dev.shape[1] != g.n or not Y_dev.is_contiguous():
+            raise ValueError("Y_dev must be a contiguous float64 [B, n] CUDA tensor")
+        if sigma2_dev.dtype != torch.float64 or sigma2_dev.numel() != B or not sigma2_dev.is_contiguous():
+            raise ValueError("sigma2_dev must be a contiguous float64 [B] CUDA tensor")
+        if workspace is None:
+            workspace, nb = _workspace(g, B)
+        else:
+            nb = workspace.numel()
+        if outputs is None:
+            outputs = self.alloc_outputs(B, Y_dev.device)
+        est, ok, its, syn = outputs
+        rc = _native.lib().ldpc_decode_awgn(g.handle, _ptr(Y_dev), _ptr(sigma2_dev), B, int(max_iterations),
+                                            _flags(early_stop, precision, schedule), _ptr(est), _ptr(ok), _ptr(its),
+                                            _ptr(syn) if syndrome_out else None, _ptr(workspace), nb,
+                                            _native.current_stream_handle(g.device), None)
+        _native.check(rc, "ldpc_decode_awgn")
         return outputs
 
     def decode_channel(self, seed: int, point: int, frame0: int, B: int, sigma2: float, max_iterations: int,
