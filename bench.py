@@ -374,10 +374,10 @@ def run_ours(args):
         Y_host, s2_y = synthetic_observations(H, B, args.ebno, seed=2000 + rank)
         Y_pin = torch.from_numpy(Y_host).pin_memory().numpy()
         for _ in range(max(1, args.warmup)):
-            dec.decode_batch(Y_pin, s2_y, iters, early_stop=False)
+            dec.decode_batch(Y_pin, s2_y, iters, early_stop=False, out=res)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            dec.decode_batch(Y_pin, s2_y, iters, early_stop=False)
+            dec.decode_batch(Y_pin, s2_y, iters, early_stop=False, out=res)
         el_y = time.perf_counter() - t0
         ty = torch.tensor([el_y], dtype=torch.float64, device=dev)
         if world > 1:

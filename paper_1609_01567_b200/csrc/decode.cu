@@ -734,7 +734,28 @@ static std::vector<int32_t> chunk_plan(int32_t B, int32_t sub) {
         const char *e = getenv("LDPC_E2E_GROWTH");
         return e ? std::max(101, atoi(e)) : 150;
     }();
+    // experiment hook: LDPC_E2E_PLAN="64,64,128,..." (sizes in order; the last one repeats)
+    static const std::vector<int32_t> fixed = [] {
+        std::vector<int32_t> f;
+        if (const char *e = getenv("LDPC_E2E_PLAN"))
+            for (const char *q = e; *q;) {
+                const int x = atoi(q);
+                if (x > 0) f.push_back(x);
+                while (*q && *q != ',') q++;
+                if (*q == ',') q++;
+            }
+        return f;
+    }();
     std::vector<int32_t> v;
+    if (!fixed.empty()) {
+        for (int32_t c0 = 0, i = 0; c0 < B; i++) {
+            int32_t take = std::min<int32_t>(fixed[std::min<size_t>(i, fixed.size() - 1)], B - c0);
+            if ((int)v.size() == kMaxChunks - 1) take = B - c0;
+            v.push_back(take);
+            c0 += take;
+        }
+        return v;
+    }
     const int32_t cap = std::max<int32_t>(64, sub / 64 * 64);
     int32_t b = std::min<int32_t>(cap, 64);
     for (int32_t c0 = 0; c0 < B;) {

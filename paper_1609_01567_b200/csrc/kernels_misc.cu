@@ -28,14 +28,18 @@ __global__ void k_transpose_priors(const double *__restrict__ in, const double *
                                    int32_t n, double *__restrict__ P, int32_t Bp) {
     __shared__ double tile[32][33];
     const int j0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
-    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
-        const int c = c0 + y, j = j0 + threadIdx.x;
-        double v = 0.5;
-        if (c < B && j < n) {
-            v = __ldcs(in + (size_t)c * n + j);
-            if (AWGN) v = awgn_prior(v, __ldg(sig2 + c));
-        }
-        tile[y][threadIdx.x] = v;
+    // blockDim (32, 8): 4 rows per thread, loads issued before any prior arithmetic
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int c = c0 + threadIdx.y + 8 * k, j = j0 + threadIdx.x;
+        v[k] = (c < B && j < n) ? __ldcs(in + (size_t)c * n + j) : 0.5;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int c = c0 + threadIdx.y + 8 * k;
+        if (AWGN && c < B && j0 + (int)threadIdx.x < n) v[k] = awgn_prior(v[k], __ldg(sig2 + c));
+        tile[threadIdx.y + 8 * k][threadIdx.x] = v[k];
     }
     __syncthreads();
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {

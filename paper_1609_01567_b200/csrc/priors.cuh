@@ -20,6 +20,8 @@
 #pragma once
 #include <cstdint>
 
+#include "common.cuh"
+
 namespace ldpc {
 
 static __device__ __forceinline__ double bits_d(uint64_t u) { return __longlong_as_double((long long)u); }
@@ -131,10 +133,17 @@ static __device__ __forceinline__ double np_exp(double x) {
     return __dmul_rn(e, bits_d((uint64_t)((int)floor(k) + 1023) << 52));
 }
 
+// IEEE division, = __ddiv_rn bit for bit (common.cuh ddiv_fast, slow path only when needed)
+static __device__ __forceinline__ double ddiv_exact(double a, double b) {
+    bool ok;
+    const double q = ddiv_fast(a, b, ok);
+    return ok ? q : __ddiv_rn(a, b);
+}
+
 // serial.py:49-50: 1.0 / (1.0 + np.exp(-2.0 * y / sigma2)), one rounding per operation
 static __device__ __forceinline__ double awgn_prior(double y, double sigma2) {
-    const double t = __ddiv_rn(__dmul_rn(-2.0, y), sigma2);
-    return __ddiv_rn(1.0, __dadd_rn(1.0, np_exp(t)));
+    const double t = ddiv_exact(__dmul_rn(-2.0, y), sigma2);
+    return ddiv_exact(1.0, __dadd_rn(1.0, np_exp(t)));
 }
 
 }  // namespace ldpc

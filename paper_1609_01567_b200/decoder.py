@@ -493,8 +493,9 @@ class ParallelDecoder:
         return self.decode_priors(p.reshape(1, -1), max_iterations)[0]
 
     def decode_batch(self, Y, sigma2, max_iterations: int = DEFAULT_MAX_ITERATIONS,
-                     early_stop: bool = True, precision: str = "fp64", schedule: str = "auto") -> BatchResult:
-        """B received frames [B, n] (sigma2 scalar or [B]) -> BatchResult."""
+                     early_stop: bool = True, precision: str = "fp64", schedule: str = "auto",
+                     out: BatchResult | None = None) -> BatchResult:
+        """B received frames [B, n] (sigma2 scalar or [B]) -> BatchResult (into ``out`` if given)."""
         if self._closed:
             raise RuntimeError("decoder is closed")
         Y = np.asarray(Y, dtype=np.float64)
@@ -507,9 +508,9 @@ class ParallelDecoder:
             # bit-identical to numpy's.  Pinned Y (torch pin_memory) copies at full speed.
             if (s2 <= 0).any():
                 raise ValueError("sigma2 must be positive")
-            return self._run(np.ascontiguousarray(Y), np.ascontiguousarray(s2), max_iterations, early_stop, None,
+            return self._run(np.ascontiguousarray(Y), np.ascontiguousarray(s2), max_iterations, early_stop, out,
                              precision, schedule)
-        res = BatchResult(np.empty((B, (n + 31) // 32), np.uint32), np.empty(B, np.uint8), np.empty(B, np.int32),
+        res = out if out is not None else BatchResult(np.empty((B, (n + 31) // 32), np.uint32), np.empty(B, np.uint8), np.empty(B, np.int32),
                           np.empty((B, (m + 31) // 32), np.uint32), n, m)
         # priors go into a reused pinned buffer (no page faults, full-speed copies), max_batch frames at a time
         buf = self._pinned_priors()
