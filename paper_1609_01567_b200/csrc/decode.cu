@@ -55,7 +55,7 @@ size_t chain_scratch_doubles(const ldpc_graph *g, int32_t Bp) {
     // per phase: every wide node of the side x its tile x the side's max degree (x2 for r and 1-r)
     size_t wide_c = 0, wide_v = 0;
     for (const Bucket &b : g->chk_buckets)
-        if (b.deg > kMaxRegDegree) wide_c += (size_t)b.node_count;
+        if (b.deg > kMaxRegCheckDegree) wide_c += (size_t)b.node_count;
     for (const Bucket &b : g->var_buckets)
         if (b.deg > kMaxRegDegree) wide_v += (size_t)b.node_count;
     size_t need = 0;
@@ -232,7 +232,7 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
     for (const Bucket &b : g->chk_buckets) {
-        if (b.deg <= kMaxRegDegree) {
+        if (b.deg <= kMaxRegCheckDegree) {
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;

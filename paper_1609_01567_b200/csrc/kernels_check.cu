@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
 }
 
 // ---- high-degree path: chains of outputs over shared-memory b ------------------
-// One block per (check, tile of TW codewords), 1024 threads; any degree.  The d outputs need
+// One block per (check, tile of TW codewords), 1024 threads; degrees past kMaxRegCheckDegree.  The d outputs need
 // d(d-1)/2 ordered multiplies per codeword (exactness forbids a suffix-product
 // shortcut), so the work is fp64-bound for d >> 16 and is spread as:
 //   * b_i = 1 - 2 q_i of the tile staged in shared memory ([d][TW]), or in the
@@ -141,9 +141,10 @@ __device__ __forceinline__ int chains_group(int w, int t) {  // t-th group of wa
     return band * 64 + ((t & 1) ? 63 - w : w);
 }
 
-template <int TW, bool FROM_PRIOR, bool GS>  // GS: staging in global scratch (degrees past the smem budget)
+// R: outputs per group (R*TW/32 chains per thread)
+template <int TW, bool FROM_PRIOR, bool GS, int R = kWideR>  // GS: staging in global scratch (degrees past the smem budget)
 __global__ void __launch_bounds__(kWideThreads) k_check_chains(NodeLaunch a, int max_deg) {
-    constexpr int CPT = kWideR * TW / 32;   // chains per thread
+    constexpr int CPT = R * TW / 32;   // chains per thread
     static_assert(CPT >= 1 && kWideThreads == 1024, "TW must be >= 4; 32 warps");
     extern __shared__ double smem_b[];
     double *b = GS ? a.scratch + (size_t)blockIdx.x * max_deg * TW : smem_b;  // [d][TW]
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kWideThreads) k_check_chains(NodeLaunch a, int
     const int node = __ldg(a.order + a.node_begin + ni);
     const int pos0 = __ldg(a.off + node);
     const int d = __ldg(a.off + node + 1) - pos0;
-    const int G = (d + kWideR - 1) / kWideR;
+    const int G = (d + R - 1) / R;
     for (int e = threadIdx.x; e < d * TW; e += blockDim.x) {
         const int i = e / TW, cc = e - i * TW;
         const int cwe = tile * TW + cc;
@@ -178,9 +179,9 @@ __global__ void __launch_bounds__(kWideThreads) k_check_chains(NodeLaunch a, int
     for (int t = 0;; t++) {
         const int g = chains_group(warp, t);
         if (g >= G) break;
-        const int k0 = g * kWideR, kb = k0 + j0;       // first output of this thread
+        const int k0 = g * R, kb = k0 + j0;            // first output of this thread
         const int gn = chains_group(warp, t + 1);
-        const int next = gn * kWideR + j0;             // where the carry must stop (next group's kb)
+        const int next = gn * R + j0;                  // where the carry must stop (next group's kb)
         for (; at < kb; at++) pre = __dmul_rn(pre, at < d ? B(at) : 1.0);
         double acc[CPT];
         double p = pre;
@@ -252,9 +253,14 @@ int launch_one(const NodeLaunch &a, cudaStream_t s) {
 
 template <int D>
 int launch_deg(const NodeLaunch &a, bool fp, cudaStream_t s) {
-    const int V = (a.Bp % 64) ? 1 : vpolicy_check(D);  // tile views of 32 codewords take V=1
-    if (V == 2) return fp ? launch_one<D, 2, true>(a, s) : launch_one<D, 2, false>(a, s);
-    return fp ? launch_one<D, 1, true>(a, s) : launch_one<D, 1, false>(a, s);
+    // tile views of 32 codewords take V=1; so do degrees past 16 (D*V values in registers)
+    if constexpr (D > kMaxRegDegree) {
+        return fp ? launch_one<D, 1, true>(a, s) : launch_one<D, 1, false>(a, s);
+    } else {
+        const int V = (a.Bp % 64) ? 1 : vpolicy_check(D);
+        if (V == 2) return fp ? launch_one<D, 2, true>(a, s) : launch_one<D, 2, false>(a, s);
+        return fp ? launch_one<D, 1, true>(a, s) : launch_one<D, 1, false>(a, s);
+    }
 }
 
 }  // namespace
@@ -265,6 +271,8 @@ int launch_check_bucket(const NodeLaunch &a, int deg, bool from_prior, cudaStrea
     case D: return launch_deg<D>(a, from_prior, s);
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
         CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+        CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24)
+        CASE(25) CASE(26) CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
 #undef CASE
         default:
             set_error("register-path check degree %d out of range", deg);
@@ -274,7 +282,15 @@ int launch_check_bucket(const NodeLaunch &a, int deg, bool from_prior, cudaStrea
 
 template <int TW, bool GS>
 int launch_chains(const NodeLaunch &a, int max_deg, size_t smem, bool from_prior, cudaStream_t s) {
+    // groups of 16 outputs (8 chains per thread at TW = 16) when they still fill the 32 warps'
+    // bands; else 8.  LDPC_CHAIN_R=8|16 forces one.
+    static const int r_env = [] {
+        const char *e = getenv("LDPC_CHAIN_R");
+        return e ? atoi(e) : 0;
+    }();
+    const bool r16 = r_env ? r_env == 16 : (max_deg + 15) / 16 >= 48;
     auto kern = from_prior ? k_check_chains<TW, true, GS> : k_check_chains<TW, false, GS>;
+    if (r16) kern = from_prior ? k_check_chains<TW, true, GS, 16> : k_check_chains<TW, false, GS, 16>;
     if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (int64_t)a.node_count * (a.Bp / TW);
     kern<<<(unsigned)blocks, kWideThreads, smem, s>>>(a, max_deg);

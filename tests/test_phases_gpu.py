@@ -236,3 +236,34 @@ def test_engine_shared_state_phases(cuda):
         assert np.array_equal(st.estimate, O.estimate(st.p, st.r))
         parallel_syndrome(st, T, plan)
         assert np.array_equal(st.syndrome, O.syndrome(st.estimate))
+
+
+@pytest.mark.parametrize("check_degrees,B", [
+    ({17: 40, 24: 40, 30: 40, 32: 40}, 70),   # register path past 16 (V = 1)
+    ({33: 30, 40: 30}, 40),                    # just past it: the chains kernel
+])
+def test_mid_check_degrees_vs_oracle(cuda, check_degrees, B):
+    # DVB-S2's high-rate codes have check degrees 18-30 (rates 4/5 .. 9/10)
+    from oracle import OracleTables
+    from paper_1609_01567_b200 import ParallelDecoder, generate_irregular_code, priors_awgn_batch
+
+    vdeg = {8: 600, 3: 900, 2: 1800}
+    E = sum(d * c for d, c in vdeg.items())
+    m = sum(check_degrees.values()) + (E - sum(d * c for d, c in check_degrees.items())) // 7
+    H = generate_irregular_code(vdeg, m, seed=21, check_degrees=check_degrees)
+    dc = H.degrees()[1]
+    for d in check_degrees:
+        assert (dc == d).sum() >= check_degrees[d]
+    T = CodeTables.from_matrix(H)
+    O = OracleTables.from_matrix(H)
+    rng = np.random.default_rng(22)
+    Q = rng.uniform(size=(3, H.total_edges))
+    assert np.array_equal(bits(values_to_variable(Q, T)), bits(np.stack([O.values_to_variable(q) for q in Q])))
+    s2 = 0.5
+    P = priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((B, H.n)), s2)
+    with ParallelDecoder(T, max_batch=B) as dec:
+        for early in (True, False):
+            res = dec.decode_priors(P, 12, early_stop=early, schedule="stream")
+            est, ok, its, z = O.decode_batch(P, 12, fixed_iterations=not early)
+            assert np.array_equal(res.estimates(), est) and np.array_equal(res.syndromes(), z)
+            assert np.array_equal(res.success.astype(bool), ok) and np.array_equal(res.iterations, its)

@@ -180,3 +180,21 @@ def test_device_api_observations(cuda):
         torch.cuda.synchronize()
         for a, b in ((est, est2), (ok, ok2), (its, its2), (syn, syn2)):
             assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
+def test_decode_observations_extreme_values(cuda):
+    """Saturated priors (p exactly 0 or 1, exp overflow), the rare exp path and subnormal exps."""
+    if not decoder_mod.device_priors_exact(0):
+        pytest.skip("host numpy exp differs from the device prior")
+    H, Y, s2 = _observations("C1", 24, 2.0, 15)
+    rng = np.random.default_rng(16)
+    mask = rng.random(Y.shape) < 0.02
+    Y[mask] = rng.choice([-400.0, -360.0, -354.2, 354.0, 360.0, 1e5, -1e5], mask.sum())
+    sig = np.full(24, s2)
+    sig[:4] = [1e-3, 0.5, 1.0, 2.0]
+    with ParallelDecoder(CodeTables.from_matrix(H), max_batch=24) as dec:
+        for schedule in ("stream", "onchip"):
+            dev = dec.decode_batch(Y, sig, 15, schedule=schedule)
+            host = dec.decode_priors(priors_awgn_batch(Y, sig), 15, schedule=schedule)
+            _assert_same(dev, host)
