@@ -129,28 +129,30 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
 //     and each thread carries CPT = R*TW/32 output chains of its group, so one
 //     shared load feeds CPT independent multiplies, and the TW lanes reading a row
 //     form a conflict-free wavefront (the 32/TW parts read the same row: broadcast);
-//   * warp w takes groups w, 63-w, 64+w, 127-w, ... : ascending (so one running
+//   * a block has W = min(32, ceil(G/2)) warps for G groups (mid degrees get small
+//     blocks, many per SM);
+//   * warp w takes groups w, 2W-1-w, 2W+w, 4W-1-w, ... : ascending (so one running
 //     prefix 1*b_0*...*b_{k-1} carried across its groups replaces a sequential
 //     prefix pass), and balanced (each band of 64 pairs a long suffix with a short
 //     one).  The carry rides in the body loop as one more chain.
 constexpr int kWideR = 8;
 constexpr int kWideThreads = 1024;
 
-__device__ __forceinline__ int chains_group(int w, int t) {  // t-th group of warp w (32 warps)
+__device__ __forceinline__ int chains_group(int w, int t, int nw) {  // t-th group of warp w (of nw)
     const int band = t >> 1;
-    return band * 64 + ((t & 1) ? 63 - w : w);
+    return band * 2 * nw + ((t & 1) ? 2 * nw - 1 - w : w);
 }
 
 // R: outputs per group (R*TW/32 chains per thread)
 template <int TW, bool FROM_PRIOR, bool GS, int R = kWideR>  // GS: staging in global scratch (degrees past the smem budget)
 __global__ void __launch_bounds__(kWideThreads) k_check_chains(NodeLaunch a, int max_deg) {
     constexpr int CPT = R * TW / 32;   // chains per thread
-    static_assert(CPT >= 1 && kWideThreads == 1024, "TW must be >= 4; 32 warps");
+    static_assert(CPT >= 1 && kWideThreads == 1024, "TW must be >= 4; up to 32 warps");
     extern __shared__ double smem_b[];
     double *b = GS ? a.scratch + (size_t)blockIdx.x * max_deg * TW : smem_b;  // [d][TW]
     const int tile = blockIdx.x / a.node_count;  // tile-major: all nodes of tile 0 first
     const int ni = blockIdx.x - tile * a.node_count;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int c = lane % TW, h = lane / TW;
     const int cw = tile * TW + c;
     if (a.done != nullptr) {
@@ -177,10 +179,10 @@ __global__ void __launch_bounds__(kWideThreads) k_check_chains(NodeLaunch a, int
     double pre = 1.0;
     int at = 0;
     for (int t = 0;; t++) {
-        const int g = chains_group(warp, t);
+        const int g = chains_group(warp, t, nw);
         if (g >= G) break;
         const int k0 = g * R, kb = k0 + j0;            // first output of this thread
-        const int gn = chains_group(warp, t + 1);
+        const int gn = chains_group(warp, t + 1, nw);
         const int next = gn * R + j0;                  // where the carry must stop (next group's kb)
         for (; at < kb; at++) pre = __dmul_rn(pre, at < d ? B(at) : 1.0);
         double acc[CPT];
@@ -280,6 +282,12 @@ int launch_check_bucket(const NodeLaunch &a, int deg, bool from_prior, cudaStrea
     }
 }
 
+// warps per block: enough for two groups each (a band pairs a long suffix with a short one), up to 32
+inline int chain_warps(int max_deg, int R) {
+    const int G = (max_deg + R - 1) / R;
+    return std::max(1, std::min(32, (G + 1) / 2));
+}
+
 template <int TW, bool GS>
 int launch_chains(const NodeLaunch &a, int max_deg, size_t smem, bool from_prior, cudaStream_t s) {
     // groups of 16 outputs (8 chains per thread at TW = 16) when they still fill the 32 warps'
@@ -293,7 +301,7 @@ int launch_chains(const NodeLaunch &a, int max_deg, size_t smem, bool from_prior
     if (r16) kern = from_prior ? k_check_chains<TW, true, GS, 16> : k_check_chains<TW, false, GS, 16>;
     if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (int64_t)a.node_count * (a.Bp / TW);
-    kern<<<(unsigned)blocks, kWideThreads, smem, s>>>(a, max_deg);
+    kern<<<(unsigned)blocks, 32 * chain_warps(max_deg, r16 ? 16 : kWideR), smem, s>>>(a, max_deg);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }

@@ -170,19 +170,19 @@ __global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_re
 }
 
 // ---- high-degree path: chains of outputs over shared-memory r / 1-r -----------
-// Same structure as k_check_chains (kernels_check.cu): one block of 1024 threads per
-// (variable, tile of TW codewords), any degree; r and 1 - r staged in shared memory
+// Same structure as k_check_chains (kernels_check.cu): one block of up to 1024 threads per
+// (variable, tile of TW codewords), degrees past 16; r and 1 - r staged in shared memory
 // (or the workspace scratch past the shared-memory budget); outputs in
 // groups of R = 8 with CPT = R*TW/32 chains per thread, each chain the pair
-// (q0, q1) of serial.py:77-88; warps take groups w, 63-w, 64+w, ... ascending so a
+// (q0, q1) of serial.py:77-88; W warps take groups w, 2W-1-w, 2W+w, ... ascending so a
 // running prefix pair ((1-p)*prod(1-r_i), p*prod(r_i)) is carried across groups.
 // Warp 0 part 0 carries its prefix to the end: the estimate's (Q0, Q1).
 constexpr int kChainR = 8;
 constexpr int kChainThreads = 1024;
 
-__device__ __forceinline__ int var_chains_group(int w, int t) {
+__device__ __forceinline__ int var_chains_group(int w, int t, int nw) {  // t-th group of warp w (of nw)
     const int band = t >> 1;
-    return band * 64 + ((t & 1) ? 63 - w : w);
+    return band * 2 * nw + ((t & 1) ? 2 * nw - 1 - w : w);
 }
 
 template <int TW, bool WRITE_Q, bool GS>  // GS: staging in global scratch (degrees past the smem budget)
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kChainThreads) k_var_chains(NodeLaunch a, int 
     double *sm = GS ? a.scratch + (size_t)blockIdx.x * max_deg * TW * 2 : smem_rs;
     const int tile = blockIdx.x / a.node_count;
     const int ni = blockIdx.x - tile * a.node_count;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int c = lane % TW, h = lane / TW;
     const int cw = tile * TW + c;
     const int w = (tile * TW) >> 5;
@@ -225,10 +225,10 @@ __global__ void __launch_bounds__(kChainThreads) k_var_chains(NodeLaunch a, int 
     if constexpr (WRITE_Q) {
         const int j0 = h * CPT;
         for (int t = 0;; t++) {
-            const int g = var_chains_group(warp, t);
+            const int g = var_chains_group(warp, t, nw);
             if (g >= G) break;
             const int kb = g * kChainR + j0;
-            const int next = var_chains_group(warp, t + 1) * kChainR + j0;
+            const int next = var_chains_group(warp, t + 1, nw) * kChainR + j0;
             for (; at < kb; at++) step(at);
             double a0[CPT], a1[CPT];
             double p0 = pre0, p1 = pre1;
@@ -313,7 +313,9 @@ int launch_var_chains(const NodeLaunch &a, int max_deg, size_t smem, bool write_
     auto kern = write_q ? k_var_chains<TW, true, GS> : k_var_chains<TW, false, GS>;
     if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (int64_t)a.node_count * (a.Bp / TW);
-    kern<<<(unsigned)blocks, kChainThreads, smem, s>>>(a, max_deg);
+    // warps: two groups each (balanced band pairs), up to 32
+    const int nw = std::max(1, std::min(32, ((max_deg + kChainR - 1) / kChainR + 1) / 2));
+    kern<<<(unsigned)blocks, 32 * nw, smem, s>>>(a, max_deg);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }

@@ -238,16 +238,17 @@ def test_engine_shared_state_phases(cuda):
         assert np.array_equal(st.syndrome, O.syndrome(st.estimate))
 
 
-@pytest.mark.parametrize("check_degrees,B", [
-    ({17: 40, 24: 40, 30: 40, 32: 40}, 70),   # register path past 16 (V = 1)
-    ({33: 30, 40: 30}, 40),                    # just past it: the chains kernel
+@pytest.mark.parametrize("check_degrees,extra_vars,B", [
+    ({17: 40, 24: 40, 30: 40, 32: 40}, {}, 70),            # register path past 16 (V = 1)
+    ({33: 30, 40: 30}, {}, 40),                            # just past it: the chains kernel
+    ({90: 8, 300: 2}, {17: 30, 33: 10, 120: 3}, 36),       # small chains blocks, both sides
 ])
-def test_mid_check_degrees_vs_oracle(cuda, check_degrees, B):
+def test_mid_degrees_vs_oracle(cuda, check_degrees, extra_vars, B):
     # DVB-S2's high-rate codes have check degrees 18-30 (rates 4/5 .. 9/10)
     from oracle import OracleTables
     from paper_1609_01567_b200 import ParallelDecoder, generate_irregular_code, priors_awgn_batch
 
-    vdeg = {8: 600, 3: 900, 2: 1800}
+    vdeg = {8: 600, 3: 900, 2: 1800, **extra_vars}
     E = sum(d * c for d, c in vdeg.items())
     m = sum(check_degrees.values()) + (E - sum(d * c for d, c in check_degrees.items())) // 7
     H = generate_irregular_code(vdeg, m, seed=21, check_degrees=check_degrees)
