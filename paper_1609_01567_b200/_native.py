@@ -88,6 +88,8 @@ def _declare(L):
     u64 = ctypes.c_uint64
     L.ldpc_channel_awgn.argtypes = [u64, u64, u64, i32, i32, ctypes.c_double, vp, vp]
     L.ldpc_channel_awgn.restype = ctypes.c_int
+    L.ldpc_channel_awgn_host.argtypes = [u64, u64, u64, i32, i32, ctypes.c_double, vp, i32]
+    L.ldpc_channel_awgn_host.restype = ctypes.c_int
     L.ldpc_decode_channel.argtypes = [vp, u64, u64, u64, i32, ctypes.c_double, i32, u32, vp, vp, vp, vp, vp, sz, vp]
     L.ldpc_decode_channel.restype = ctypes.c_int
     L.ldpc_phase_f32.argtypes = [vp, ctypes.c_int, vp, vp, vp, i32, vp, sz, vp]

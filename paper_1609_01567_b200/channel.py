@@ -12,11 +12,13 @@ iterations, frames} per point.  Integer sums are exact, so the BerPoints are
 identical for any number of ranks (and to the single-process reference).
 
 Channel arithmetic: the integer RNG is exact.  ``exact_channel=True`` runs
-Box-Muller with Python's math functions element by element, exactly like
+Box-Muller with the same libm calls as Python's math module, in C on host
+threads (csrc/host_channel.cpp, ``transmit_all_zero_frames``), exactly like
 channel.py:31-37, so y -- and with the bit-exact decoder the whole BerPoint --
 equals the reference's.  The default vectorised path uses numpy's log/cos/sin,
 which may differ from libm in the last ulp (statistically identical noise, not
-bit-identical; the reference's channel arithmetic is itself untested).
+bit-identical; the reference's channel arithmetic is itself untested).  ber_sweep
+uses the exact native channel by default.
 """
 
 from __future__ import annotations
@@ -170,6 +172,28 @@ def transmit_all_zero_batch(n: int, sigma2: float, states: list[RngState], exact
     return -1.0 + math.sqrt(sigma2) * z[:, :n]
 
 
+def transmit_all_zero_frames(n: int, sigma2: float, seed: int, point: int, frame0: int, count: int,
+                             threads: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+    """Frames frame0..frame0+count-1 of Eb/N0 point ``point`` ([count, n]), each from
+    derive_state(seed, point, frame) (channel.py:112), bit-identical to transmit_all_zero
+    (the same libm log/cos/sin calls; csrc/host_channel.cpp), on ``threads`` host threads."""
+    import ctypes
+
+    from . import _native
+
+    if sigma2 <= 0.0:
+        raise ValueError("sigma2 must be positive")
+    if out is None:
+        out = np.empty((count, n), dtype=np.float64)
+    elif out.shape != (count, n) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous float64 [count, n] array")
+    rc = _native.load_library().ldpc_channel_awgn_host(int(seed) & MASK64, int(point) & MASK64,
+                                                        int(frame0) & MASK64, int(count), int(n), float(sigma2),
+                                                        ctypes.c_void_p(out.ctypes.data), int(threads))
+    _native.check(rc, "ldpc_channel_awgn_host")
+    return out
+
+
 # ---- channel.py:70-148 ------------------------------------------------------
 
 @dataclass(frozen=True)
@@ -205,10 +229,18 @@ def gpu_decode_counts(decoder, early_stop: bool = True, precision: str = "fp64")
 
     from .decoder import priors_awgn_batch
 
+    from .decoder import device_priors_exact
+
     def run(Y, sigma2, max_iterations, counts):
-        P = torch.from_numpy(priors_awgn_batch(Y, sigma2)).to(counts.device)
-        outs = decoder.decode_device(P, max_iterations, early_stop=early_stop, syndrome_out=False,
-                                     precision=precision)
+        if device_priors_exact(counts.device.index or 0):   # priors formed on the device, bit-identical
+            Yd = torch.from_numpy(np.ascontiguousarray(Y)).to(counts.device)
+            S = torch.full((Yd.shape[0],), float(sigma2), dtype=torch.float64, device=counts.device)
+            outs = decoder.decode_device_awgn(Yd, S, max_iterations, early_stop=early_stop, syndrome_out=False,
+                                              precision=precision)
+        else:
+            P = torch.from_numpy(priors_awgn_batch(Y, sigma2)).to(counts.device)
+            outs = decoder.decode_device(P, max_iterations, early_stop=early_stop, syndrome_out=False,
+                                         precision=precision)
         decoder.count_errors(outs, counts)
 
     return run
@@ -216,7 +248,7 @@ def gpu_decode_counts(decoder, early_stop: bool = True, precision: str = "fp64")
 
 def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int = 0, group_size: int = 512,
               decoders_in_flight: int = 1, rate: float | None = None, *, batch: int = DEFAULT_BATCH, decode_fn=None,
-              exact_channel: bool = False, device=None, channel: str = "host",
+              exact_channel: bool = True, device=None, channel: str = "host",
               precision: str = "fp64", early_stop: bool = True) -> list[BerPoint]:
     """channel.py:83-137 on the GPU, frames sharded over torch.distributed ranks.
 
@@ -226,8 +258,9 @@ def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int =
     decode_fn(Y [b, n], sigma2, max_iterations, counts) must add
     [bit errors, failures, iterations, frames] of the batch into the int64[4]
     tensor ``counts``; the default decodes on this rank's GPU.
-    exact_channel=True draws the noise with the reference's scalar math (bit-identical
-    BerPoints); the default vectorised channel is statistically identical.
+    exact_channel=True (default) draws the noise with the reference's scalar math in C on
+    host threads (bit-identical BerPoints); False uses numpy's vectorised log/cos/sin
+    (statistically identical noise).
     channel="device" (f1) generates the noise and priors on the GPU as well
     (integer-exact RNG streams, device transcendentals: statistical parity).
     precision="fp32" selects the fast mode; early_stop=False runs every frame for max_iterations
@@ -266,8 +299,11 @@ def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int =
             counts = torch.zeros(4, dtype=torch.int64, device=device)
             for b0 in range(lo, hi, batch):
                 fr = range(b0, min(hi, b0 + batch))
-                states = [derive_state(seed, index, f) for f in fr]   # channel.py:112
-                Y = transmit_all_zero_batch(H.n, sigma2, states, exact=exact_channel)
+                if exact_channel:   # the reference's channel bit for bit, native threads
+                    Y = transmit_all_zero_frames(H.n, sigma2, seed, index, b0, len(fr))
+                else:
+                    states = [derive_state(seed, index, f) for f in fr]   # channel.py:112
+                    Y = transmit_all_zero_batch(H.n, sigma2, states)
                 decode_fn(Y, sigma2, max_iterations, counts)
             if dist is not None:
                 dist.all_reduce(counts)                                # the only collective

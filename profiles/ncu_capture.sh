@@ -27,7 +27,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_on
     -o $OUT/prof_${TAG}_onchip python bench.py --config C1 --batch 1 --iters 50 --steps 1 --warmup 0 --no-e2e \
     --no-cpu --no-configs --no-fast > $OUT/ncu_onchip_$TAG.log 2>&1
 echo "onchip capture rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_transpose_priors -c 2 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_transpose_priors -s 20 -c 2 \
     -o $OUT/prof_${TAG}_priors python tools/prior_kernel_probe.py > $OUT/ncu_priors_$TAG.log 2>&1
 echo "priors capture rc=$?"
 ls -la $OUT

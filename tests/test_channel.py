@@ -41,6 +41,25 @@ def test_exact_channel_matches_reference(gch):
     assert np.array_equal(Y.view(np.uint64), gch["channel/y_h96_seed5"].view(np.uint64))
 
 
+def test_native_channel_matches_reference(gch):
+    # csrc/host_channel.cpp: the reference's scalar channel (libm log/cos/sin) in C, on threads
+    Y = ch.transmit_all_zero_frames(96, 0.63, seed=5, point=0, frame0=0, count=6, threads=3)
+    assert np.array_equal(Y.view(np.uint64), gch["channel/y_h96_seed5"].view(np.uint64))
+
+
+@pytest.mark.parametrize("n,point,frame0,threads", [(101, 2, 7, 1), (64800 // 8 + 1, 3, 1000, 4), (1, 0, 0, 0)])
+def test_native_channel_matches_scalar_path(n, point, frame0, threads):
+    Y = ch.transmit_all_zero_frames(n, 0.7943, seed=11, point=point, frame0=frame0, count=5, threads=threads)
+    for i in range(5):
+        want = ch.transmit_all_zero(n, 0.7943, ch.derive_state(11, point, frame0 + i))[1]
+        assert np.array_equal(Y[i].view(np.uint64), want.view(np.uint64))
+
+
+def test_native_channel_rejects_bad_sigma2():
+    with pytest.raises(ValueError):
+        ch.transmit_all_zero_frames(8, 0.0, 1, 0, 0, 2)
+
+
 def test_vectorised_uniforms_are_exact():
     states = [ch.derive_state(3, 1, f) for f in range(5)]
     U = ch.uniforms_batch(states, 40)
