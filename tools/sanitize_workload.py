@@ -1,7 +1,9 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): every kernel
 family on tiny inputs -- graph build, streaming decode (check register kernel, variable ring kernels,
 syndrome, done flags, layout), on-chip decode (1 CTA and a 2-CTA cluster), high-degree chains
-kernels, fp32 fast mode, the phase API, the host and streaming decoders, the device channel."""
+kernels (1024-thread and small blocks), the register check path past degree 16, fp32 fast mode,
+the phase API, the host and streaming decoders, the device channel, device priors from observations
+(fused layout kernel, on-chip, standalone exp/prior kernels)."""
 import sys
 
 import numpy as np
@@ -43,5 +45,24 @@ with ParallelDecoder(CodeTables.from_matrix(H2), max_batch=2) as dec:
 H4 = generate_irregular_code({200: 2, 3: 3000, 2: 3000}, 2000, seed=5, check_degrees={600: 2})
 with ParallelDecoder(CodeTables.from_matrix(H4), max_batch=2) as dec:
     dec.decode_priors(priors(H4, 2, 1.5, 6), 2, early_stop=False)
+# check degrees 17-32 (register path, V = 1) and 33-40 / variable 17-40 (small chains blocks)
+H5 = generate_irregular_code({40: 4, 20: 8, 8: 300, 3: 400, 2: 800}, 700, seed=7,
+                             check_degrees={24: 10, 32: 10, 36: 4, 40: 4})
+with ParallelDecoder(CodeTables.from_matrix(H5), max_batch=3) as dec:
+    dec.decode_priors(priors(H5, 3, 1.5, 8), 3, early_stop=True)
+# observations in: fused prior in the layout kernel, on chip, standalone kernels
+s2 = configs.ebno_to_sigma2(1.5, configs.rate(H1))
+Y = -1.0 + np.sqrt(s2) * rng.standard_normal((8, H1.n))
+Y[0, :4] = [400.0, -400.0, 1e5, -1e5]
+with ParallelDecoder(T1, max_batch=8) as dec:
+    for sched in ("stream", "onchip"):
+        dec.decode_batch(Y, s2, 4, schedule=sched)
+    dec.decode_batch_async(Y, s2, 3).wait()
+from paper_1609_01567_b200 import _native  # noqa: E402
+Yd = torch.from_numpy(Y).to(dev)
+Sd = torch.full((8,), s2, dtype=torch.float64, device=dev)
+Pd = torch.empty_like(Yd)
+_native.check(_native.lib().ldpc_priors_awgn(Yd.data_ptr(), Sd.data_ptr(), 8, H1.n, Pd.data_ptr(), None), "priors")
+_native.check(_native.lib().ldpc_npexp(Yd.data_ptr(), Yd.numel(), Pd.data_ptr(), None), "npexp")
 torch.cuda.synchronize()
 print("sanitize workload done")
