@@ -164,12 +164,29 @@ __global__ void __launch_bounds__(kWideThreads) k_check_chains(NodeLaunch a, int
     const int pos0 = __ldg(a.off + node);
     const int d = __ldg(a.off + node + 1) - pos0;
     const int G = (d + R - 1) / R;
-    for (int e = threadIdx.x; e < d * TW; e += blockDim.x) {
-        const int i = e / TW, cc = e - i * TW;
-        const int cwe = tile * TW + cc;
-        const double q = FROM_PRIOR ? __ldg(a.P + cofs(a.p_rows, __ldg(a.idx + pos0 + i), cwe))
-                                    : ld_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + i) : pos0 + i, cwe));
-        b[e] = __dsub_rn(1.0, __dmul_rn(2.0, q));
+    if constexpr (!GS) {
+        // the tile's d row segments (TW codewords, 16-byte pieces) all in flight at once
+        // (cp.async, no register round trip), then b = 1 - 2q in place
+        constexpr int PPR = TW / 2;  // pieces per row segment
+        for (int e = threadIdx.x; e < d * PPR; e += blockDim.x) {
+            const int i = e / PPR, pc = e - i * PPR;
+            const int cwe = tile * TW + 2 * pc;
+            const double *src = FROM_PRIOR ? a.P + cofs(a.p_rows, __ldg(a.idx + pos0 + i), cwe)
+                                           : a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + i) : pos0 + i, cwe);
+            cp_async16(b + i * TW + 2 * pc, src);
+        }
+        cp_commit();
+        cp_wait<0>();
+        __syncthreads();
+        for (int e = threadIdx.x; e < d * TW; e += blockDim.x) b[e] = __dsub_rn(1.0, __dmul_rn(2.0, b[e]));
+    } else {
+        for (int e = threadIdx.x; e < d * TW; e += blockDim.x) {
+            const int i = e / TW, cc = e - i * TW;
+            const int cwe = tile * TW + cc;
+            const double q = FROM_PRIOR ? __ldg(a.P + cofs(a.p_rows, __ldg(a.idx + pos0 + i), cwe))
+                                        : ld_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + pos0 + i) : pos0 + i, cwe));
+            b[e] = __dsub_rn(1.0, __dmul_rn(2.0, q));
+        }
     }
     __syncthreads();
     const double *bc = b + c;

@@ -205,13 +205,27 @@ __global__ void __launch_bounds__(kChainThreads) k_var_chains(NodeLaunch a, int 
     const int G = (d + kChainR - 1) / kChainR;
     double *rs = sm;                    // [d][TW] r_i
     double *os = sm + (size_t)d * TW;   // [d][TW] 1 - r_i
-    for (int e = threadIdx.x; e < d * TW; e += blockDim.x) {
-        const int i = e / TW, cc = e - i * TW;
-        const double r = ld_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + e0 + i) : e0 + i, tile * TW + cc));
-        rs[e] = r;
-        os[e] = __dsub_rn(1.0, r);
-    }
     const double pj = __ldg(a.P + cofs(a.p_rows, node, cw));
+    if constexpr (!GS) {
+        // the tile's d row segments all in flight at once (cp.async), then 1 - r
+        constexpr int PPR = TW / 2;  // 16-byte pieces per row segment
+        for (int e = threadIdx.x; e < d * PPR; e += blockDim.x) {
+            const int i = e / PPR, pc = e - i * PPR;
+            cp_async16(rs + i * TW + 2 * pc,
+                       a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + e0 + i) : e0 + i, tile * TW + 2 * pc));
+        }
+        cp_commit();
+        cp_wait<0>();
+        __syncthreads();
+        for (int e = threadIdx.x; e < d * TW; e += blockDim.x) os[e] = __dsub_rn(1.0, rs[e]);
+    } else {
+        for (int e = threadIdx.x; e < d * TW; e += blockDim.x) {
+            const int i = e / TW, cc = e - i * TW;
+            const double r = ld_msg(a.msg + cofs(a.msg_rows, a.slot ? __ldg(a.slot + e0 + i) : e0 + i, tile * TW + cc));
+            rs[e] = r;
+            os[e] = __dsub_rn(1.0, r);
+        }
+    }
     __syncthreads();
     const double *rc = rs + c, *oc = os + c;
     double pre0 = __dsub_rn(1.0, pj), pre1 = pj;  // running prefix pair over positions < at
