@@ -27,6 +27,7 @@ FLAG_FIXED_ITERS = 1
 FLAG_FP32 = 2
 FLAG_STREAMING = 4
 FLAG_ONCHIP = 8
+FLAG_GRID = 16
 
 VARIABLE = 0
 CHECK = 1

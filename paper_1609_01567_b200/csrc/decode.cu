@@ -395,6 +395,17 @@ extern "C" size_t ldpc_workspace_bytes(const ldpc_graph *g, int32_t B) {
     return workspace_bytes(g, B);
 }
 
+// grid schedule by default for B <= kGridMaxB while its working set stays well inside the L2
+// (LDPC_GRID=0 disables the automatic choice)
+constexpr size_t kGridAutoBytes = 64ull << 20;
+static bool grid_auto() {
+    static const bool on = [] {
+        const char *e = getenv("LDPC_GRID");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // p_dev: priors [B][n]; or, with sig2 != nullptr, observations y [B][n] whose priors are
 // formed inside the layout transpose (priors.cuh).
 static int decode_impl(const ldpc_graph *g, const double *p_dev, const double *sig2, int32_t B, int32_t max_iterations,
@@ -405,16 +416,24 @@ static int decode_impl(const ldpc_graph *g, const double *p_dev, const double *s
     DeviceGuard dg(g->device);
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
     LDPC_ARG_CHECK(p_dev && est_bits_dev && success_dev && iters_dev, "NULL output/input pointer");
-    LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32 | LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP)) == 0,
+    LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32 | LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP |
+                              LDPC_FLAG_GRID)) == 0,
                    "unknown flags 0x%x", flags);
     const bool fast = (flags & LDPC_FLAG_FP32) != 0;
     LDPC_ARG_CHECK(!fast || (g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree),
                    "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
+    LDPC_ARG_CHECK(__builtin_popcount(flags & (LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP | LDPC_FLAG_GRID)) <= 1,
+                   "at most one schedule flag");
     cudaStream_t s = (cudaStream_t)stream;
     const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
+    // a few codewords of a code too large for the on-chip schedule: one cooperative launch (grid.cu)
+    const bool want_grid = (flags & LDPC_FLAG_GRID) != 0;
+    LDPC_ARG_CHECK(!want_grid || (!fast && grid_suitable(g, B)),
+                   "the grid schedule takes 1..%d codewords of a code with node degrees <= %d (fp64)", kGridMaxB,
+                   kMaxRegDegree);
     // small codes: the whole decode on chip (onchip.cu), unless the caller forces streaming
     const bool want_onchip = (flags & LDPC_FLAG_ONCHIP) != 0;
-    const int cs = (fast || (flags & LDPC_FLAG_STREAMING)) ? 0
+    const int cs = (fast || (flags & (LDPC_FLAG_STREAMING | LDPC_FLAG_GRID))) ? 0
                    : want_onchip ? onchip_cluster_size(g, true) : (onchip_auto(g, B) ? 1 : 0);
     LDPC_ARG_CHECK(!(flags & LDPC_FLAG_ONCHIP) || (cs > 0 && !(flags & LDPC_FLAG_STREAMING)),
                    "the on-chip schedule needs a code whose messages fit 8 CTAs' shared memory (fp64)");
@@ -422,6 +441,12 @@ static int decode_impl(const ldpc_graph *g, const double *p_dev, const double *s
         LDPC_ARG_CHECK(B >= 1, "batch must be at least 1");
         return launch_onchip(g, cs, p_dev, sig2, B, max_iterations, early, est_bits_dev, success_dev, iters_dev,
                              syn_bits_dev, s);
+    }
+    if (prof_host == nullptr && !fast && !(flags & (LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP)) &&
+        (want_grid || (grid_auto() && grid_suitable(g, B) && grid_workspace_bytes(g, B) <= kGridAutoBytes))) {
+        LDPC_ARG_CHECK(workspace_dev != nullptr, "NULL workspace");
+        return launch_grid(g, p_dev, sig2, B, max_iterations, early, est_bits_dev, success_dev, iters_dev,
+                           syn_bits_dev, workspace_dev, workspace_bytes_, s);
     }
     Workspace w;
     int rc = carve_workspace(g, B, workspace_dev, workspace_bytes_, &w);

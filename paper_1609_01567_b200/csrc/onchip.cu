@@ -37,6 +37,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "nodes.cuh"
 #include "priors.cuh"
 
 namespace cg = cooperative_groups;
@@ -112,145 +113,6 @@ __device__ __forceinline__ void cluster_barrier() {
     }
 }
 
-// check-node update of check `c` (serial.py:92-112); prior-fed pre-pass when FROM_PRIOR
-template <int CS, bool FROM_PRIOR>
-__device__ __forceinline__ void check_update(const Cl<CS> &cl, int c) {
-    const OnchipArgs &a = *cl.a;
-    const int s0 = __ldg(a.chk_off + c), d = __ldg(a.chk_off + c + 1) - s0;
-    auto bval = [&](int i) {
-        const double q = FROM_PRIOR ? cl.prior_of(__ldg(a.chk_var + s0 + i)) : *cl.slot(s0 + i);
-        return __dsub_rn(1.0, __dmul_rn(2.0, q));
-    };
-    double pre = 1.0;
-    for (int k = 0; k < d; k++) {
-        double acc = pre;
-        for (int i = k + 1; i < d; i++) acc = __dmul_rn(acc, bval(i));
-        pre = __dmul_rn(pre, bval(k));  // slot k's q is read before r_k overwrites it
-        *cl.slot(s0 + k) = __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc)));
-    }
-}
-
-// variable-node update + estimate of the variable at var_order position `pos`
-// (serial.py:63-89, 115-133); returns the hard decision
-template <int CS>
-__device__ __forceinline__ uint8_t var_update(const Cl<CS> &cl, int pos, bool write_q, double pj) {
-    const OnchipArgs &a = *cl.a;
-    const int v = __ldg(a.var_order + pos);
-    const int e0 = __ldg(a.var_off + v), d = __ldg(a.var_off + v + 1) - e0;
-    double pre0 = __dsub_rn(1.0, pj), pre1 = pj;
-    for (int k = 0; k < d; k++) {
-        double *sk = cl.slot(__ldg(a.var_pos + e0 + k));
-        const double rk = *sk;
-        if (write_q) {
-            double q0 = pre0, q1 = pre1;
-            for (int i = k + 1; i < d; i++) {
-                const double ri = *cl.slot(__ldg(a.var_pos + e0 + i));
-                q0 = __dmul_rn(q0, __dsub_rn(1.0, ri));
-                q1 = __dmul_rn(q1, ri);
-            }
-            pre0 = __dmul_rn(pre0, __dsub_rn(1.0, rk));
-            pre1 = __dmul_rn(pre1, rk);
-            const double den = __dadd_rn(q0, q1);
-            bool ok;
-            double q = ddiv_fast(q1, den, ok);
-            if (!ok) q = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
-            *sk = q;  // r_k was read into the prefix first
-        } else {
-            pre0 = __dmul_rn(pre0, __dsub_rn(1.0, rk));
-            pre1 = __dmul_rn(pre1, rk);
-        }
-    }
-    return (pre0 > pre1) ? 0 : 1;
-}
-
-// Degree-specialised node updates: the d inputs are gathered into registers first
-// (independent shared / DSMEM loads overlap their latency), then the same
-// arithmetic as the streaming register kernels; outputs go back through the
-// same pointers (each slot is read before any output of the node is stored).
-template <int CS, int D, bool FROM_PRIOR>
-__device__ __forceinline__ void check_update_d(const Cl<CS> &cl, int s0) {
-    const OnchipArgs &a = *cl.a;
-    double *ptr[D];
-    double b[D];
-#pragma unroll
-    for (int i = 0; i < D; i++) {
-        ptr[i] = cl.slot(s0 + i);
-        const double q = FROM_PRIOR ? cl.prior_of(__ldg(a.chk_var + s0 + i)) : *ptr[i];
-        b[i] = __dsub_rn(1.0, __dmul_rn(2.0, q));
-    }
-    double pre = 1.0;
-#pragma unroll
-    for (int k = 0; k < D; k++) {
-        double acc = pre;
-#pragma unroll
-        for (int i = k + 1; i < D; i++) acc = __dmul_rn(acc, b[i]);
-        *ptr[k] = __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc)));
-        if (k + 1 < D) pre = __dmul_rn(pre, b[k]);
-    }
-}
-
-template <int CS, int D>
-__device__ __forceinline__ uint8_t var_update_d(const Cl<CS> &cl, int e0, bool write_q, double pj) {
-    const OnchipArgs &a = *cl.a;
-    double *ptr[D];
-    double r[D], om[D];
-#pragma unroll
-    for (int i = 0; i < D; i++) {
-        ptr[i] = cl.slot(__ldg(a.var_pos + e0 + i));
-        r[i] = *ptr[i];
-        om[i] = __dsub_rn(1.0, r[i]);
-    }
-    double p0 = __dsub_rn(1.0, pj), p1 = pj;
-#pragma unroll
-    for (int k = 0; k < D; k++) {
-        if (write_q) {
-            double q0 = p0, q1 = p1;
-#pragma unroll
-            for (int i = k + 1; i < D; i++) {
-                q0 = __dmul_rn(q0, om[i]);
-                q1 = __dmul_rn(q1, r[i]);
-            }
-            const double den = __dadd_rn(q0, q1);
-            bool ok;
-            double q = ddiv_fast(q1, den, ok);
-            if (!ok) q = (den == 0.0) ? 0.5 : __ddiv_rn(q1, den);
-            *ptr[k] = q;
-        }
-        p0 = __dmul_rn(p0, om[k]);
-        p1 = __dmul_rn(p1, r[k]);
-    }
-    return (p0 > p1) ? 0 : 1;
-}
-
-template <int CS, bool FROM_PRIOR>
-__device__ __forceinline__ void check_node(const Cl<CS> &cl, int c) {
-    const OnchipArgs &a = *cl.a;
-    const int s0 = __ldg(a.chk_off + c), d = __ldg(a.chk_off + c + 1) - s0;
-    switch (d) {
-#define CASE(D) \
-    case D: check_update_d<CS, D, FROM_PRIOR>(cl, s0); return;
-        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-        default: check_update<CS, FROM_PRIOR>(cl, c);
-    }
-}
-
-template <int CS>
-__device__ __forceinline__ uint8_t var_node(const Cl<CS> &cl, int pos, bool write_q, double pj) {
-    const OnchipArgs &a = *cl.a;
-    const int v = __ldg(a.var_order + pos);
-    const int e0 = __ldg(a.var_off + v), d = __ldg(a.var_off + v + 1) - e0;
-    switch (d) {
-#define CASE(D) \
-    case D: return var_update_d<CS, D>(cl, e0, write_q, pj);
-        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-        default: return var_update<CS>(cl, pos, write_q, pj);
-    }
-}
-
 // shared-memory layout of a rank: [erow RWn u32][zrow 2 x RWm u32][flag 4 int] (a fixed-size header,
 // so rank 0's output rows sit at the same offset in every rank's view) | msg | p | chat
 __host__ __device__ __forceinline__ size_t onchip_header(int RWn, int RWm) {
@@ -307,6 +169,7 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const __grid_constant
     __syncthreads();
     const int c0 = a.cb[rank], c1 = a.cb[rank + 1];
     const int v0 = a.vb[rank];
+    const NodeTables tb{a.chk_off, a.chk_var, a.var_off, a.var_pos};
 
     for (int cw = cid; cw < a.B; cw += nclusters) {
         // priors of this rank's variables (serial.py:58: q = p[v] feeds the pre-pass)
@@ -325,14 +188,15 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const __grid_constant
         }
         cluster_barrier<CS>();
         // pre-pass C-phase from the priors (serial.py:166)
-        for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) check_node<CS, true>(cl, __ldg(a.chk_list + i));
+        for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) check_node<true>(cl, tb, __ldg(a.chk_list + i));
         cluster_barrier<CS>();
         int t = 0;
         bool success = false;
         for (;; t++) {
             const bool more = t < a.max_iter;
             // VE: estimate of round t and, unless this is the last round, q for round t+1
-            for (int i = threadIdx.x; i < nvars; i += blockDim.x) chat[i] = var_node<CS>(cl, v0 + i, more, pl[i]);
+            for (int i = threadIdx.x; i < nvars; i += blockDim.x)
+                chat[i] = var_node(cl, tb, __ldg(a.var_order + v0 + i), more, pl[i]);
             cluster_barrier<CS>();
             // SC: syndrome of round t (+ its bits) and r for round t+1.  The other parity's flag and
             // syndrome row were last read / written before the VE barrier: reset them for round t+1.
@@ -348,7 +212,7 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const __grid_constant
                 for (int k = 0; k < d; k++) z ^= cl.chat_of(__ldg(a.chk_var + s0 + k));
                 unsat |= z;
                 if (z && a.syn) atomicOr(zr + (c >> 5), 1u << (c & 31));
-                if (more) check_node<CS, false>(cl, c);
+                if (more) check_node<false>(cl, tb, c);
             }
             if (__syncthreads_or(unsat) && threadIdx.x == 0) flag[t & 1] = 1;
             cluster_barrier<CS>();

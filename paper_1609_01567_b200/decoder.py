@@ -223,12 +223,13 @@ def _dev(a: np.ndarray, device: int):
 
 # ---- single phases (serial.py:63-147 signatures, any batch) -------------------
 
-SCHEDULES = ("auto", "stream", "onchip")
+SCHEDULES = ("auto", "stream", "onchip", "grid")
 
 
 def _flags(early_stop: bool, precision: str, schedule: str = "auto") -> int:
     """schedule: "auto" decodes small codes entirely on chip (one CTA or thread-block cluster per
-    codeword, onchip.cu) and streams the rest; "stream" / "onchip" force one (identical results)."""
+    codeword, onchip.cu), a few codewords of larger codes in one cooperative launch (grid.cu), and
+    streams the rest; "stream" / "onchip" / "grid" force one (identical results)."""
     if precision not in ("fp64", "fp32"):
         raise ValueError("precision must be 'fp64' (exact) or 'fp32' (fast mode)")
     if schedule not in SCHEDULES:
@@ -236,7 +237,8 @@ def _flags(early_stop: bool, precision: str, schedule: str = "auto") -> int:
     return ((_native.FLAG_EARLY_STOP if early_stop else _native.FLAG_FIXED_ITERS)
             | (_native.FLAG_FP32 if precision == "fp32" else 0)
             | (_native.FLAG_STREAMING if schedule == "stream" else 0)
-            | (_native.FLAG_ONCHIP if schedule == "onchip" else 0))
+            | (_native.FLAG_ONCHIP if schedule == "onchip" else 0)
+            | (_native.FLAG_GRID if schedule == "grid" else 0))
 
 
 def values_to_check(p, r, tables: CodeTables, precision: str = "fp64") -> np.ndarray:
