@@ -455,6 +455,23 @@ def run_ours(args):
                             "coded_Gbit_s": B_o * H_o.n / (ms_o / 1e3) / 1e9, "mean_iterations": its_o,
                             "n": H_o.n, "edges": H_o.total_edges}
             del P_o, ws_o, outs_o
+        # the reference-facing single-frame call at C3 (engine.py:363 decode(y, sigma2)): host in,
+        # host out, wall clock; one cooperative grid launch per frame (grid.cu)
+        Y1, s2_1 = synthetic_observations(H, 12, args.ebno, seed=77)
+        with ParallelDecoder(T, max_batch=1) as d1:
+            for y in Y1[:3]:
+                d1.decode(y, s2_1, 50)
+            lat, its1 = [], []
+            for y in Y1[3:]:
+                t0 = time.perf_counter()
+                r1 = d1.decode(y, s2_1, 50)
+                lat.append(time.perf_counter() - t0)
+                its1.append(r1.iterations_used)
+        others["C3_single_frame"] = {"batch": 1, "max_iterations": 50, "early_stop": True,
+                                     "ms_per_decode_wall": 1e3 * float(np.median(lat)),
+                                     "mean_iterations": float(np.mean(its1)),
+                                     "path": "ParallelDecoder.decode(y, sigma2): H2D of y, device prior, "
+                                             "grid schedule (one cooperative launch), D2H"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
