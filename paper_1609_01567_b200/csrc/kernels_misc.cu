@@ -60,7 +60,15 @@ __global__ void k_syndrome(const int32_t *__restrict__ chk_off, const int32_t *_
         for (int i = blockIdx.x * 8 + threadIdx.y; i < m; i += gridDim.x * 8) {
             const int a = __ldg(chk_off + i), b = __ldg(chk_off + i + 1);
             uint32_t z = 0;
-            for (int p = a; p < b; p++) z ^= chat[(size_t)__ldg(chk_var + p) * NWs + w];
+            // 8 independent loads in flight per step (a long check would otherwise pay one
+            // dependent L2 round trip per variable)
+            for (int p = a; p < b; p += 8) {
+                uint32_t x[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) x[u] = (p + u < b) ? chat[(size_t)__ldg(chk_var + p + u) * NWs + w] : 0u;
+#pragma unroll
+                for (int u = 0; u < 8; u++) z ^= x[u];
+            }
             if (zb != nullptr) zb[(size_t)i * NWs + w] = z;
             acc |= z;
         }

@@ -40,7 +40,8 @@ constexpr int ring_stages(int rows) {
     return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
-// Per stage: 32 row ids (one per lane), the task's codeword chunk at [32], pad to 16 bytes.
+// Per stage: 32 row ids (one per lane), the task's codeword chunk at [32], its skip flag at [33]
+// and its done-mask words at [34..35] (early stop: read with the ids, two issues ahead).
 constexpr int kIdsStride = 36;
 template <int ROWS, int V, int MINB>
 struct Ring {
@@ -67,16 +68,27 @@ __device__ __forceinline__ void ld_smem(const double *p, double (&o)[V]) {
     }
 }
 
-// all codewords of warp-chunk ch (32*V codewords) have stopped
+
+// done-mask words of warp-chunk ch (0 when not in early-stop mode), read ahead of the task
+struct DoneMask {
+    uint32_t w0 = 0, w1 = 0;
+};
 template <int V>
-__device__ __forceinline__ bool wchunk_done(const uint32_t *done, int ch) {
-    if (done == nullptr) return false;
+__device__ __forceinline__ DoneMask load_done(const uint32_t *done, int ch) {
+    DoneMask m;
+    if (done == nullptr) return m;
     if constexpr (V == 2) {
         const uint2 d = *reinterpret_cast<const uint2 *>(done + 2 * ch);
-        return (d.x & d.y) == 0xffffffffu;
+        m.w0 = d.x;
+        m.w1 = d.y;
     } else {
-        return done[ch] == 0xffffffffu;
+        m.w0 = done[ch];
     }
+    return m;
+}
+template <int V>
+__device__ __forceinline__ bool all_done(const DoneMask &m) {
+    return V == 2 ? (m.w0 & m.w1) == 0xffffffffu : m.w0 == 0xffffffffu;
 }
 
 // Row ids of a task, one per lane:
@@ -105,13 +117,20 @@ template <int D, bool IS_VAR>
 constexpr int ring_rows() { return D + (prior_in_ring<D, IS_VAR>() ? 1 : 0); }
 
 template <int D, int V, bool IS_VAR, bool FROM_PRIOR>
-__device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *ids_s, int ch, int id, int lane) {
+__device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *ids_s, int ch, int id,
+                                      const DoneMask &dm, int lane) {
     constexpr int ROWS = ring_rows<D, IS_VAR>();
     constexpr int ROW = 32 * V;                 // doubles per row
     constexpr int RPI = V == 2 ? 1 : 2;         // rows per copy instruction
+    const bool skip = all_done<V>(dm);
     ids_s[lane] = id;
-    if (lane == 0) ids_s[32] = ch;
-    if (wchunk_done<V>(a.done, ch)) return;  // nothing to fetch; compute skips it too
+    if (lane == 0) {
+        ids_s[32] = ch;
+        ids_s[33] = skip ? 1 : 0;
+        ids_s[34] = (int)dm.w0;
+        ids_s[35] = (int)dm.w1;
+    }
+    if (skip) return;  // every codeword of the chunk has stopped: nothing to fetch; compute skips it too
     const int cw0 = ch * 32 * V;
     const int sub = V == 2 ? 0 : (lane >> 4);  // which row of the instruction's pair this lane copies
     const int piece = V == 2 ? lane : (lane & 15);
@@ -242,20 +261,16 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
             uint32_t lo = part1by1(even) | (part1by1(odd) << 1);
             uint32_t hi = part1by1(even >> 16) | (part1by1(odd >> 16) << 1);
             uint32_t *dst = row + 2 * ch;
-            if (a.done != nullptr) {
-                const uint32_t d0 = a.done[2 * ch], d1 = a.done[2 * ch + 1];
-                if (d0) lo = (lo & ~d0) | (dst[0] & d0);
-                if (d1) hi = (hi & ~d1) | (dst[1] & d1);
-            }
+            const uint32_t d0 = (uint32_t)ids[34], d1 = (uint32_t)ids[35];  // prefetched done mask
+            if (d0) lo = (lo & ~d0) | (dst[0] & d0);
+            if (d1) hi = (hi & ~d1) | (dst[1] & d1);
             *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
         }
     } else {
         uint32_t bits = __ballot_sync(0xffffffffu, !(p0[0] > p1[0]));
         if (lane == 0) {
-            if (a.done != nullptr) {
-                const uint32_t d0 = a.done[ch];
-                if (d0) bits = (bits & ~d0) | (row[ch] & d0);
-            }
+            const uint32_t d0 = (uint32_t)ids[34];  // prefetched done mask
+            if (d0) bits = (bits & ~d0) | (row[ch] & d0);
             row[ch] = bits;
         }
     }
@@ -298,24 +313,30 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
     const int chunks_m1 = a.Bp / (32 * V) - 1;  // reverse sweep: chunk c -> chunks-1-c
     auto chunk_of = [&](int c) { return a.reverse ? chunks_m1 - c : c; };
     int nid0 = load_id<D, IS_VAR, FP>(a, cur.ni, lane), nch0 = chunk_of(cur.ch);
+    DoneMask nd0 = load_done<V>(a.done, nch0);
     cur.next();
     int nid1 = 0, nch1 = 0;
+    DoneMask nd1;
     if (ntask > 1) {
         nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
         nch1 = chunk_of(cur.ch);
+        nd1 = load_done<V>(a.done, nch1);
         cur.next();
     }
     auto issue_next = [&](int j) {  // issue task j (j < ntask) into stage j % S
         const int id = nid0, ich = nch0;
+        const DoneMask idone = nd0;
         nid0 = nid1;
         nch0 = nch1;
+        nd0 = nd1;
         if (j + 2 < ntask) {
             nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
             nch1 = chunk_of(cur.ch);
+            nd1 = load_done<V>(a.done, nch1);
             cur.next();
         }
         const int sj = j % S;
-        issue<D, V, IS_VAR, FP>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, lane);
+        issue<D, V, IS_VAR, FP>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, idone, lane);
     };
     // prologue: copies of tasks 0..S-2 (one commit group per task)
     for (int j = 0; j < S - 1; j++) {
@@ -358,7 +379,7 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
         } else if constexpr (IS_VAR) {
             ld_smem<V>(rows + (size_t)s * ROWS * ROW + D * ROW + V * lane, pj);
         }
-        if (!wchunk_done<V>(a.done, ch)) {
+        if (!ids_s[33]) {
             if constexpr (IS_VAR) compute_var<D, V, FLAG>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane, pj);
             else compute_check<D, V>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane);
         }
