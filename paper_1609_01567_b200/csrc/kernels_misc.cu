@@ -7,6 +7,8 @@
 // reference, engine.py:324-326, "about 34% of decode time" in the paper) is an
 // OR-reduction of z over checks: per thread in registers, per block in shared
 // memory, then one atomicOr per word per block.
+#include <algorithm>
+
 #include "common.cuh"
 #include "priors.cuh"
 
@@ -48,10 +50,12 @@ __global__ void k_transpose_priors(const double *__restrict__ in, const double *
     }
 }
 
+constexpr int kLongSyndrome = 64;  // checks of higher degree: one block per (check, word), k_syndrome_long
+
 // blockDim (32, 8): x -> word, y -> check; grid (check slabs, word groups)
 __global__ void k_syndrome(const int32_t *__restrict__ chk_off, const int32_t *__restrict__ chk_var, int32_t m,
                            const uint32_t *__restrict__ chat, int32_t NW, int32_t NWs, uint32_t *__restrict__ zb,
-                           uint32_t *__restrict__ unsat, const uint32_t *__restrict__ done) {
+                           uint32_t *__restrict__ unsat, const uint32_t *__restrict__ done, int skip_long) {
     __shared__ uint32_t red[8][32];
     const int w = blockIdx.y * 32 + threadIdx.x;
     uint32_t acc = 0;
@@ -59,6 +63,7 @@ __global__ void k_syndrome(const int32_t *__restrict__ chk_off, const int32_t *_
     if (live) {
         for (int i = blockIdx.x * 8 + threadIdx.y; i < m; i += gridDim.x * 8) {
             const int a = __ldg(chk_off + i), b = __ldg(chk_off + i + 1);
+            if (skip_long && b - a > kLongSyndrome) continue;  // k_syndrome_long
             uint32_t z = 0;
             // 8 independent loads in flight per step (a long check would otherwise pay one
             // dependent L2 round trip per variable)
@@ -82,6 +87,33 @@ __global__ void k_syndrome(const int32_t *__restrict__ chk_off, const int32_t *_
 #pragma unroll
         for (int y = 0; y < 8; y++) o |= red[y][threadIdx.x];
         if (o & ~unsat[w]) atomicOr(unsat + w, o);
+    }
+}
+
+// Syndrome words of the long checks chk_order[first ..]: block (check, word), 256 threads over
+// the check's variables, XOR-reduced through shuffles and shared memory (one round trip
+// instead of one per variable).
+__global__ void k_syndrome_long(const int32_t *__restrict__ chk_off, const int32_t *__restrict__ chk_var,
+                                const int32_t *__restrict__ chk_order, int32_t first, const uint32_t *__restrict__ chat,
+                                int32_t NWs, uint32_t *__restrict__ zb, uint32_t *__restrict__ unsat,
+                                const uint32_t *__restrict__ done) {
+    __shared__ uint32_t red[8];
+    const int c = __ldg(chk_order + first + blockIdx.x);
+    const int w = blockIdx.y;
+    const bool live = !(done != nullptr && done[w] == 0xffffffffu);
+    uint32_t z = 0;
+    if (live) {
+        const int a = __ldg(chk_off + c), b = __ldg(chk_off + c + 1);
+        for (int p = a + threadIdx.x; p < b; p += blockDim.x) z ^= chat[(size_t)__ldg(chk_var + p) * NWs + w];
+        for (int o = 16; o > 0; o >>= 1) z ^= __shfl_xor_sync(0xffffffffu, z, o);
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = z;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++) t ^= red[k];
+        if (zb != nullptr) zb[(size_t)c * NWs + w] = t;
+        if (t & ~unsat[w]) atomicOr(unsat + w, t);
     }
 }
 
@@ -234,11 +266,21 @@ int launch_transpose_priors(const double *p_in, const double *sig2, int32_t B, i
 }
 
 int launch_syndrome(const ldpc_graph *g, const Workspace &w, bool write_z, bool use_done, cudaStream_t s) {
+    // checks past kLongSyndrome: a suffix of chk_order (sorted by degree), one block per (check, word)
+    int32_t first_long = g->m;
+    for (const Bucket &b : g->chk_buckets)
+        if (b.deg > kLongSyndrome) first_long = std::min(first_long, b.node_begin);
     const unsigned gx = blocks_for(g->m, 8, 148 * 8);
     dim3 grid(gx, (w.NW + 31) / 32);
     k_syndrome<<<grid, dim3(32, 8), 0, s>>>(g->chk_off, g->chk_var, g->m, w.chat, w.NW, w.NWs, write_z ? w.zb : nullptr,
-                                             w.unsat, use_done ? w.done : nullptr);
+                                             w.unsat, use_done ? w.done : nullptr, first_long < g->m ? 1 : 0);
     LDPC_CHECK_LAUNCH();
+    if (first_long < g->m) {
+        k_syndrome_long<<<dim3(g->m - first_long, w.NW), 256, 0, s>>>(
+            g->chk_off, g->chk_var, g->chk_order, first_long, w.chat, w.NWs, write_z ? w.zb : nullptr, w.unsat,
+            use_done ? w.done : nullptr);
+        LDPC_CHECK_LAUNCH();
+    }
     return LDPC_OK;
 }
 
