@@ -64,5 +64,13 @@ Sd = torch.full((8,), s2, dtype=torch.float64, device=dev)
 Pd = torch.empty_like(Yd)
 _native.check(_native.lib().ldpc_priors_awgn(Yd.data_ptr(), Sd.data_ptr(), 8, H1.n, Pd.data_ptr(), None), "priors")
 _native.check(_native.lib().ldpc_npexp(Yd.data_ptr(), Yd.numel(), Pd.data_ptr(), None), "npexp")
+# grid schedule (cooperative launch), early and fixed; long-check syndrome (degree 600 checks, early stop)
+H6 = configs.code("C2")
+with ParallelDecoder(CodeTables.from_matrix(H6), max_batch=3) as dec:
+    P6 = priors(H6, 3, 1.5, 9)
+    dec.decode_priors(P6, 6, schedule="grid")
+    dec.decode_priors(P6, 4, early_stop=False, schedule="grid")
+with ParallelDecoder(CodeTables.from_matrix(H4), max_batch=2) as dec:
+    dec.decode_priors(priors(H4, 2, 1.5, 10), 2, early_stop=True, schedule="stream")
 torch.cuda.synchronize()
 print("sanitize workload done")
