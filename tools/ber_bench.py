@@ -31,8 +31,9 @@ if world > 1:
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 H = configs.code("C5")
 frames = args.frames_per_gpu * world
-ch.ber_sweep(H, args.ebno[:1], min(frames, 1024 * world), max_iterations=args.iters, batch=1024, channel="device",
-             precision=args.precision)  # warm-up: same precision and batch (kernel setup, graph capture)
+for _ in range(2):  # warm-up: same precision, batch and frames (kernel setup; GPU clocks up from idle)
+    ch.ber_sweep(H, args.ebno[:1], frames, max_iterations=args.iters, batch=1024, channel="device",
+                 precision=args.precision)
 torch.cuda.synchronize()
 if world > 1:
     dist.barrier()
