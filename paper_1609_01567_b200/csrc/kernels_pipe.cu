@@ -69,6 +69,18 @@ __device__ __forceinline__ void ld_smem(const double *p, double (&o)[V]) {
 }
 
 
+// all codewords of warp-chunk ch (32*V codewords) have stopped
+template <int V>
+__device__ __forceinline__ bool wchunk_done(const uint32_t *done, int ch) {
+    if (done == nullptr) return false;
+    if constexpr (V == 2) {
+        const uint2 d = *reinterpret_cast<const uint2 *>(done + 2 * ch);
+        return (d.x & d.y) == 0xffffffffu;
+    } else {
+        return done[ch] == 0xffffffffu;
+    }
+}
+
 // done-mask words of warp-chunk ch (0 when not in early-stop mode), read ahead of the task
 struct DoneMask {
     uint32_t w0 = 0, w1 = 0;
@@ -116,21 +128,26 @@ constexpr bool prior_in_ring() { return IS_VAR && D < kPriorRegDeg; }
 template <int D, bool IS_VAR>
 constexpr int ring_rows() { return D + (prior_in_ring<D, IS_VAR>() ? 1 : 0); }
 
-template <int D, int V, bool IS_VAR, bool FROM_PRIOR>
+template <int D, int V, bool IS_VAR, bool FROM_PRIOR, bool EARLY>
 __device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *ids_s, int ch, int id,
                                       const DoneMask &dm, int lane) {
     constexpr int ROWS = ring_rows<D, IS_VAR>();
     constexpr int ROW = 32 * V;                 // doubles per row
     constexpr int RPI = V == 2 ? 1 : 2;         // rows per copy instruction
-    const bool skip = all_done<V>(dm);
+    const bool skip = EARLY && all_done<V>(dm);
     ids_s[lane] = id;
     if (lane == 0) {
         ids_s[32] = ch;
-        ids_s[33] = skip ? 1 : 0;
-        ids_s[34] = (int)dm.w0;
-        ids_s[35] = (int)dm.w1;
+        if constexpr (EARLY) {
+            ids_s[33] = skip ? 1 : 0;
+            ids_s[34] = (int)dm.w0;
+            ids_s[35] = (int)dm.w1;
+        }
     }
     if (skip) return;  // every codeword of the chunk has stopped: nothing to fetch; compute skips it too
+    if constexpr (!EARLY) {
+        if (wchunk_done<V>(a.done, ch)) return;  // (a.done is null here: the fixed-iteration kernel's code)
+    }
     const int cw0 = ch * 32 * V;
     const int sub = V == 2 ? 0 : (lane >> 4);  // which row of the instruction's pair this lane copies
     const int piece = V == 2 ? lane : (lane & 15);
@@ -183,7 +200,7 @@ __device__ __forceinline__ void compute_check(const NodeLaunch &a, const double 
     }
 }
 
-template <int D, int V, bool WRITE_Q>
+template <int D, int V, bool WRITE_Q, bool EARLY>
 __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *rows, const int *ids, int ch,
                                             int lane, const double (&pj)[V]) {
     constexpr int ROW = 32 * V;
@@ -261,16 +278,20 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
             uint32_t lo = part1by1(even) | (part1by1(odd) << 1);
             uint32_t hi = part1by1(even >> 16) | (part1by1(odd >> 16) << 1);
             uint32_t *dst = row + 2 * ch;
-            const uint32_t d0 = (uint32_t)ids[34], d1 = (uint32_t)ids[35];  // prefetched done mask
-            if (d0) lo = (lo & ~d0) | (dst[0] & d0);
-            if (d1) hi = (hi & ~d1) | (dst[1] & d1);
+            if constexpr (EARLY) {
+                const uint32_t d0 = (uint32_t)ids[34], d1 = (uint32_t)ids[35];  // prefetched done mask
+                if (d0) lo = (lo & ~d0) | (dst[0] & d0);
+                if (d1) hi = (hi & ~d1) | (dst[1] & d1);
+            }
             *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
         }
     } else {
         uint32_t bits = __ballot_sync(0xffffffffu, !(p0[0] > p1[0]));
         if (lane == 0) {
-            const uint32_t d0 = (uint32_t)ids[34];  // prefetched done mask
-            if (d0) bits = (bits & ~d0) | (row[ch] & d0);
+            if constexpr (EARLY) {
+                const uint32_t d0 = (uint32_t)ids[34];  // prefetched done mask
+                if (d0) bits = (bits & ~d0) | (row[ch] & d0);
+            }
             row[ch] = bits;
         }
     }
@@ -289,7 +310,8 @@ __device__ __forceinline__ void load_prior(const NodeLaunch &a, int node, int ch
     }
 }
 
-template <int D, int V, bool IS_VAR, bool FLAG, int MINB>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
+// EARLY: early-stop mode (a.done != nullptr): per-task chunk-done masks, read ahead with the ids
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY>  // FLAG: FROM_PRIOR / WRITE_Q
 __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, int64_t first, int64_t W,
                                           unsigned char *wsm) {
     // one warp's persistent task loop: tasks first, first + W, ... of a side's bucket,
@@ -313,14 +335,14 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
     const int chunks_m1 = a.Bp / (32 * V) - 1;  // reverse sweep: chunk c -> chunks-1-c
     auto chunk_of = [&](int c) { return a.reverse ? chunks_m1 - c : c; };
     int nid0 = load_id<D, IS_VAR, FP>(a, cur.ni, lane), nch0 = chunk_of(cur.ch);
-    DoneMask nd0 = load_done<V>(a.done, nch0);
+    DoneMask nd0 = EARLY ? load_done<V>(a.done, nch0) : DoneMask{};
     cur.next();
     int nid1 = 0, nch1 = 0;
     DoneMask nd1;
     if (ntask > 1) {
         nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
         nch1 = chunk_of(cur.ch);
-        nd1 = load_done<V>(a.done, nch1);
+        if (EARLY) nd1 = load_done<V>(a.done, nch1);
         cur.next();
     }
     auto issue_next = [&](int j) {  // issue task j (j < ntask) into stage j % S
@@ -332,11 +354,11 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
         if (j + 2 < ntask) {
             nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
             nch1 = chunk_of(cur.ch);
-            nd1 = load_done<V>(a.done, nch1);
+            if (EARLY) nd1 = load_done<V>(a.done, nch1);
             cur.next();
         }
         const int sj = j % S;
-        issue<D, V, IS_VAR, FP>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, idone, lane);
+        issue<D, V, IS_VAR, FP, EARLY>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, idone, lane);
     };
     // prologue: copies of tasks 0..S-2 (one commit group per task)
     for (int j = 0; j < S - 1; j++) {
@@ -379,8 +401,8 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
         } else if constexpr (IS_VAR) {
             ld_smem<V>(rows + (size_t)s * ROWS * ROW + D * ROW + V * lane, pj);
         }
-        if (!ids_s[33]) {
-            if constexpr (IS_VAR) compute_var<D, V, FLAG>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane, pj);
+        if (EARLY ? !ids_s[33] : !wchunk_done<V>(a.done, ch)) {
+            if constexpr (IS_VAR) compute_var<D, V, FLAG, EARLY>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane, pj);
             else compute_check<D, V>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane);
         }
         __syncwarp();  // stage s is reused by the issue of the next iteration
@@ -388,12 +410,12 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
     cp_wait<0>();
 }
 
-template <int D, int V, bool IS_VAR, bool FLAG, int MINB>  // FLAG: FROM_PRIOR for checks, WRITE_Q for variables
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY>  // FLAG: FROM_PRIOR / WRITE_Q
 __global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int64_t ntasks) {
     using R = Ring<ring_rows<D, IS_VAR>(), V, MINB>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5;
-    ring_loop<D, V, IS_VAR, FLAG, MINB>(a, ntasks, (int64_t)blockIdx.x * kWarpsPerBlock + warp,
+    ring_loop<D, V, IS_VAR, FLAG, MINB, EARLY>(a, ntasks, (int64_t)blockIdx.x * kWarpsPerBlock + warp,
                                         (int64_t)gridDim.x * kWarpsPerBlock, smem + (size_t)warp * R::kBytes);
 }
 
@@ -409,11 +431,11 @@ int ring_v(bool var_side, int deg) {
     return var_side && deg >= 3 ? 1 : 2;
 }
 
-template <int D, int V, bool IS_VAR, bool FLAG, int MINB>
-int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY>
+int launch_ring_ve(const NodeLaunch &a, cudaStream_t st) {
     constexpr int ROWS = ring_rows<D, IS_VAR>();
     const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS, V, MINB>::kBytes;
-    auto kern = k_node_ring<D, V, IS_VAR, FLAG, MINB>;
+    auto kern = k_node_ring<D, V, IS_VAR, FLAG, MINB, EARLY>;
     // the shared-memory attribute is per device: set it (and size the grid) once per device
     constexpr int kMaxDevices = 64;
     static int per_sm_of[kMaxDevices] = {}, sms_of[kMaxDevices] = {};
@@ -445,6 +467,16 @@ int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
     kern<<<(unsigned)blocks, kThreads, smem, st>>>(a, ntasks);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
+}
+
+// variables get a fixed-iteration instantiation without the early-stop bookkeeping; checks
+// (ring only on request) keep the one that handles both modes
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB>
+int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
+    if constexpr (IS_VAR) {
+        if (a.done == nullptr) return launch_ring_ve<D, V, IS_VAR, FLAG, MINB, false>(a, st);
+    }
+    return launch_ring_ve<D, V, IS_VAR, FLAG, MINB, true>(a, st);
 }
 
 // Resident blocks per SM (sets the ring depth): 2 for V=2, 3 for V=1 by default;
