@@ -27,7 +27,6 @@ import os
 import pathlib
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
