@@ -198,3 +198,19 @@ def test_decode_observations_extreme_values(cuda):
             dev = dec.decode_batch(Y, sig, 15, schedule=schedule)
             host = dec.decode_priors(priors_awgn_batch(Y, sig), 15, schedule=schedule)
             _assert_same(dev, host)
+
+
+@pytest.mark.gpu
+def test_decode_observations_nonfinite(cuda):
+    """NaN / inf observations: the device prior propagates them exactly like numpy's."""
+    if not decoder_mod.device_priors_exact(0):
+        pytest.skip("host numpy exp differs from the device prior")
+    H, Y, s2 = _observations("C1", 6, 2.0, 17)
+    Y[0, :3] = [np.nan, np.inf, -np.inf]
+    Y[1, 5] = np.nan
+    Y[2, 7:9] = [np.inf, np.inf]
+    with ParallelDecoder(CodeTables.from_matrix(H), max_batch=6) as dec:
+        for schedule in ("stream", "onchip", "grid"):
+            with np.errstate(all="ignore"):
+                host = dec.decode_priors(priors_awgn_batch(Y, s2), 10, schedule=schedule)
+            _assert_same(dec.decode_batch(Y, s2, 10, schedule=schedule), host)
