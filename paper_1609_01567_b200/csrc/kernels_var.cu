@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kChainThreads) k_var_chains(NodeLaunch a, int 
                 pre1 = __dmul_rn(pre1, x1);
             }
             if (i > at) at = i;
+#pragma unroll 4
             for (; i < d; i++) {
                 const double x0 = oc[i * TW], x1 = rc[i * TW];
 #pragma unroll
