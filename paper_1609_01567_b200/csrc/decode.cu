@@ -57,7 +57,7 @@ size_t chain_scratch_doubles(const ldpc_graph *g, int32_t Bp) {
     for (const Bucket &b : g->chk_buckets)
         if (b.deg > kMaxRegCheckDegree) wide_c += (size_t)b.node_count;
     for (const Bucket &b : g->var_buckets)
-        if (b.deg > kMaxRegDegree) wide_v += (size_t)b.node_count;
+        if (b.deg > kMaxMidVarDegree) wide_v += (size_t)b.node_count;
     size_t need = 0;
     if ((size_t)g->max_dc * kChainTW * sizeof(double) > kChainSmemBudget)
         need = std::max(need, wide_c * (size_t)g->max_dc * (size_t)Bp);
@@ -269,13 +269,14 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
     for (const Bucket &b : g->var_buckets) {
-        if (b.deg <= kMaxRegDegree) {
+        if (b.deg <= kMaxMidVarDegree) {
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
             a.reverse = alt_sweep() ? ((g_sweep ^= 1) ^ 1) : 0;
-            int rc = use_ring(true, b.deg) ? launch_var_pipe(a, b.deg, write_q, s)
-                                        : launch_var_bucket(a, b.deg, write_q, s);
+            int rc = b.deg > kMaxRegDegree     ? launch_var_mid(a, b.deg, write_q, s)
+                     : use_ring(true, b.deg) ? launch_var_pipe(a, b.deg, write_q, s)
+                                             : launch_var_bucket(a, b.deg, write_q, s);
             if (rc) return rc;
         } else {
             if (wide_begin < 0) wide_begin = b.node_begin;
@@ -370,7 +371,7 @@ static int32_t tile_groups(const ldpc_graph *g, const Workspace &w, bool fast) {
 // The decode proper on a carved workspace whose P is filled.
 int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s, Prof &prof,
                bool fast = false) {
-    int rc = init_flags(w, early, s, g->n, g->max_dv > kMaxRegDegree);
+    int rc = init_flags(w, early, s, g->n, g->max_dv > kMaxMidVarDegree);
     if (rc) return rc;
     if (fast) {
         rc = launch_priors_to_f32(w.P, prior32(g, w), (size_t)g->n * w.Bp, s);

@@ -1,0 +1,140 @@
+// kernels_varmid.cu -- variable nodes of degree 17..32 (e.g. the heavy columns of 5G-NR-like
+// codes): the register kernels' data movement with the arithmetic read from shared memory.
+//
+// Past degree 16, holding r and 1-r of every edge in registers (the register / ring kernels)
+// needs ~255 registers, and the block-per-(node, tile) chains kernels are issue-bound at these
+// degrees.  Here a warp takes (variable, 32 codewords), lane = codeword, as the register
+// kernels do: its d message rows (256 bytes each) are copied with cp.async into the warp's
+// shared memory (all in flight at once, no register destination), then each lane computes
+// its codeword's d outputs in groups of G from its shared-memory column:
+//   output k = k0 + j of group k0: (1-p) (1-r_0)...(1-r_{k-1}) [running prefix]
+//              * (1-r_{k+1}) ... (1-r_{k0+G-1})                  [head, inside the group]
+//              * (1-r_{k0+G}) ... (1-r_{d-1})                     [body, shared loads]
+// (and the same with p, r_i), i.e. the reference's left-to-right products skipping edge k
+// (serial.py:77-88), one rounding per operation; q = q1 / (q0 + q1) by the exact division of
+// common.cuh, 0.5 when the denominator is zero.  The full prefix is the estimate's
+// (Q0, Q1) (serial.py:125-132).
+#include "common.cuh"
+
+namespace ldpc {
+namespace {
+
+constexpr int kMidG = 4;            // outputs per group (chains per lane)
+constexpr int kMidWarps = 8;        // warps per block
+constexpr int kMidMaxDeg = 32;
+
+template <bool WRITE_Q, bool EARLY>
+__global__ void __launch_bounds__(32 * kMidWarps) k_var_mid(NodeLaunch a, int D) {
+    extern __shared__ __align__(16) double mid_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int ni = blockIdx.x * kMidWarps + warp;
+    if (ni >= a.node_count) return;
+    uint32_t dmask = 0;
+    if constexpr (EARLY) {
+        dmask = a.done[ch];
+        if (dmask == 0xffffffffu) return;
+    }
+    double *rows = mid_smem + (size_t)warp * kMidMaxDeg * 32;  // [D][32]: row i, column = codeword
+    const int cw0 = ch * 32;
+    const int node = __ldg(a.order + a.node_begin + ni);
+    const int id = lane < D ? __ldg(a.slot_ord + a.edge_begin + ni * D + lane) : 0;
+    const double *mb_src = chunk_base(a.msg, a.msg_rows, cw0);
+    // row i (32 doubles = 256 bytes) is 16 pieces of 16 bytes: lanes 0-15 copy row 2j, 16-31 row 2j+1
+    const int sub = lane >> 4, piece = lane & 15;
+    for (int j = 0; j < (D + 1) / 2; j++) {
+        const int r = 2 * j + sub;
+        const int src = __shfl_sync(0xffffffffu, id, r < D ? r : D - 1);
+        if (r < D) cp_async16(rows + r * 32 + 2 * piece, mb_src + row_off(src) + 2 * piece);
+    }
+    cp_commit();
+    const double pj = __ldg(chunk_base(a.P, a.p_rows, cw0) + lane + row_off(node));
+    cp_wait<0>();
+    __syncwarp();
+    const double *col = rows + lane;
+    double *mb = chunk_base(a.msg, a.msg_rows, cw0) + lane;
+    double p0 = __dsub_rn(1.0, pj), p1 = pj;  // running prefix over positions < k0
+    for (int k0 = 0; k0 < D; k0 += kMidG) {
+        double a0[kMidG], a1[kMidG];
+        double q0 = p0, q1 = p1;
+#pragma unroll
+        for (int j = 0; j < kMidG; j++) {
+            a0[j] = q0;
+            a1[j] = q1;
+            if (k0 + j < D) {
+                const double r = col[(k0 + j) * 32];
+                q0 = __dmul_rn(q0, __dsub_rn(1.0, r));
+                q1 = __dmul_rn(q1, r);
+            }
+        }
+        p0 = q0;  // prefix through the group (the estimate's products at the end)
+        p1 = q1;
+        if (!WRITE_Q) continue;
+#pragma unroll
+        for (int jj = 1; jj < kMidG; jj++) {  // head: positions inside the group after each output
+            if (k0 + jj < D) {
+                const double r = col[(k0 + jj) * 32], om = __dsub_rn(1.0, r);
+#pragma unroll
+                for (int j = 0; j < jj; j++) {
+                    a0[j] = __dmul_rn(a0[j], om);
+                    a1[j] = __dmul_rn(a1[j], r);
+                }
+            }
+        }
+#pragma unroll 4
+        for (int i = k0 + kMidG; i < D; i++) {  // body
+            const double r = col[i * 32], om = __dsub_rn(1.0, r);
+#pragma unroll
+            for (int j = 0; j < kMidG; j++) {
+                a0[j] = __dmul_rn(a0[j], om);
+                a1[j] = __dmul_rn(a1[j], r);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kMidG; j++) {
+            const int k = k0 + j;
+            const int slot = __shfl_sync(0xffffffffu, id, k < D ? k : 0);
+            if (k < D) {
+                const double den = __dadd_rn(a0[j], a1[j]);
+                bool ok;
+                double q = ddiv_fast(a1[j], den, ok);
+                if (!ok) q = (den == 0.0) ? 0.5 : __ddiv_rn(a1[j], den);
+                st_msg(mb + row_off(slot), q);
+            }
+        }
+    }
+    // estimate (serial.py:132): bit = !(Q0 > Q1); bits of stopped codewords stay frozen
+    uint32_t bits = __ballot_sync(0xffffffffu, !(p0 > p1));
+    if (lane == 0) {
+        uint32_t *dst = a.chat + (size_t)node * a.NW + ch;
+        if (EARLY && dmask) bits = (bits & ~dmask) | (*dst & dmask);
+        *dst = bits;
+    }
+}
+
+template <bool WQ, bool EARLY>
+int launch_mid(const NodeLaunch &a, int deg, cudaStream_t s) {
+    const size_t smem = (size_t)kMidWarps * kMidMaxDeg * 32 * sizeof(double);
+    auto kern = k_var_mid<WQ, EARLY>;
+    static bool attr = false;  // per process: one device attribute setting suffices for these sizes
+    if (!attr) {
+        LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const dim3 grid((a.node_count + kMidWarps - 1) / kMidWarps, a.Bp / 32);
+    LDPC_ARG_CHECK(grid.y <= 65535u, "batch too large for one launch (%d codewords)", a.Bp);
+    kern<<<grid, 32 * kMidWarps, smem, s>>>(a, deg);
+    LDPC_CHECK_LAUNCH();
+    return LDPC_OK;
+}
+
+}  // namespace
+
+int launch_var_mid(const NodeLaunch &a, int deg, bool write_q, cudaStream_t s) {
+    LDPC_ARG_CHECK(deg > 0 && deg <= kMidMaxDeg, "mid-degree variable kernel takes degrees up to %d", kMidMaxDeg);
+    if (a.node_count == 0) return LDPC_OK;
+    if (a.done != nullptr) return write_q ? launch_mid<true, true>(a, deg, s) : launch_mid<false, true>(a, deg, s);
+    return write_q ? launch_mid<true, false>(a, deg, s) : launch_mid<false, false>(a, deg, s);
+}
+
+}  // namespace ldpc

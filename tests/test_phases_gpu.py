@@ -242,6 +242,7 @@ def test_engine_shared_state_phases(cuda):
     ({17: 40, 24: 40, 30: 40, 32: 40}, {}, 70),            # register path past 16 (V = 1)
     ({33: 30, 40: 30}, {}, 40),                            # just past it: the chains kernel
     ({90: 8, 300: 2}, {17: 30, 33: 10, 120: 3}, 36),       # small chains blocks, both sides
+    ({}, {20: 20, 24: 20, 30: 10, 32: 5}, 70),              # variable degrees 17-32: kernels_varmid.cu
 ])
 def test_mid_degrees_vs_oracle(cuda, check_degrees, extra_vars, B):
     # DVB-S2's high-rate codes have check degrees 18-30 (rates 4/5 .. 9/10)
