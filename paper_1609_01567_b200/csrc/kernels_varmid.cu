@@ -19,7 +19,7 @@
 namespace ldpc {
 namespace {
 
-constexpr int kMidG = 4;            // outputs per group (chains per lane)
+constexpr int kMidG = 8;            // outputs per group (chains per lane)
 constexpr int kMidWarps = 8;        // warps per block
 constexpr int kMidMaxDeg = 32;
 
@@ -116,10 +116,13 @@ template <bool WQ, bool EARLY>
 int launch_mid(const NodeLaunch &a, int deg, cudaStream_t s) {
     const size_t smem = (size_t)kMidWarps * kMidMaxDeg * 32 * sizeof(double);
     auto kern = k_var_mid<WQ, EARLY>;
-    static bool attr = false;  // per process: one device attribute setting suffices for these sizes
-    if (!attr) {
+    static bool attr[64] = {};  // the shared-memory attribute is per device
+    int dev = 0;
+    LDPC_CUDA_TRY(cudaGetDevice(&dev));
+    LDPC_ARG_CHECK(dev >= 0 && dev < 64, "device ordinal %d out of range", dev);
+    if (!attr[dev]) {
         LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr[dev] = true;
     }
     const dim3 grid((a.node_count + kMidWarps - 1) / kMidWarps, a.Bp / 32);
     LDPC_ARG_CHECK(grid.y <= 65535u, "batch too large for one launch (%d codewords)", a.Bp);
