@@ -1,4 +1,4 @@
-// kernels_varmid.cu -- variable nodes of degree 17..32 (e.g. the heavy columns of 5G-NR-like
+// kernels_varmid.cu -- variable nodes of degree 17..64 (e.g. the heavy columns of 5G-NR-like
 // codes): the register kernels' data movement with the arithmetic read from shared memory.
 //
 // Past degree 16, holding r and 1-r of every edge in registers (the register / ring kernels)
@@ -19,12 +19,14 @@
 namespace ldpc {
 namespace {
 
-constexpr int kMidG = 8;            // outputs per group (chains per lane)
-constexpr int kMidWarps = 8;        // warps per block
-constexpr int kMidMaxDeg = 32;
+constexpr int kMidG = 8;  // outputs per group (chains per lane)
+// per-warp stage of MAXD rows x 256 bytes; 8 warps per block up to degree 32 (64 KB), 4 past it
+template <int MAXD>
+constexpr int mid_warps() { return MAXD <= 32 ? 8 : 4; }
 
-template <bool WRITE_Q, bool EARLY>
-__global__ void __launch_bounds__(32 * kMidWarps) k_var_mid(NodeLaunch a, int D) {
+template <bool WRITE_Q, bool EARLY, int MAXD>
+__global__ void __launch_bounds__(32 * mid_warps<MAXD>()) k_var_mid(NodeLaunch a, int D) {
+    constexpr int kMidWarps = mid_warps<MAXD>();
     extern __shared__ __align__(16) double mid_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
@@ -35,16 +37,25 @@ __global__ void __launch_bounds__(32 * kMidWarps) k_var_mid(NodeLaunch a, int D)
         dmask = a.done[ch];
         if (dmask == 0xffffffffu) return;
     }
-    double *rows = mid_smem + (size_t)warp * kMidMaxDeg * 32;  // [D][32]: row i, column = codeword
+    double *rows = mid_smem + (size_t)warp * MAXD * 32;  // [D][32]: row i, column = codeword
     const int cw0 = ch * 32;
     const int node = __ldg(a.order + a.node_begin + ni);
-    const int id = lane < D ? __ldg(a.slot_ord + a.edge_begin + ni * D + lane) : 0;
+    // slot of edge i: lane i (< 32) holds id0, lane i - 32 holds id1 (degrees past 32)
+    const int32_t *sl = a.slot_ord + a.edge_begin + ni * D;
+    const int id0 = lane < D ? __ldg(sl + lane) : 0;
+    const int id1 = (MAXD > 32 && lane + 32 < D) ? __ldg(sl + lane + 32) : 0;
+    auto slot_of = [&](int i) {  // every lane calls it (shuffles); i may differ per lane
+        const int x0 = __shfl_sync(0xffffffffu, id0, i & 31);
+        if constexpr (MAXD <= 32) return x0;
+        const int x1 = __shfl_sync(0xffffffffu, id1, i & 31);
+        return i < 32 ? x0 : x1;
+    };
     const double *mb_src = chunk_base(a.msg, a.msg_rows, cw0);
     // row i (32 doubles = 256 bytes) is 16 pieces of 16 bytes: lanes 0-15 copy row 2j, 16-31 row 2j+1
     const int sub = lane >> 4, piece = lane & 15;
     for (int j = 0; j < (D + 1) / 2; j++) {
         const int r = 2 * j + sub;
-        const int src = __shfl_sync(0xffffffffu, id, r < D ? r : D - 1);
+        const int src = slot_of(r < D ? r : D - 1);
         if (r < D) cp_async16(rows + r * 32 + 2 * piece, mb_src + row_off(src) + 2 * piece);
     }
     cp_commit();
@@ -93,7 +104,7 @@ __global__ void __launch_bounds__(32 * kMidWarps) k_var_mid(NodeLaunch a, int D)
 #pragma unroll
         for (int j = 0; j < kMidG; j++) {
             const int k = k0 + j;
-            const int slot = __shfl_sync(0xffffffffu, id, k < D ? k : 0);
+            const int slot = slot_of(k < D ? k : 0);
             if (k < D) {
                 const double den = __dadd_rn(a0[j], a1[j]);
                 bool ok;
@@ -112,10 +123,11 @@ __global__ void __launch_bounds__(32 * kMidWarps) k_var_mid(NodeLaunch a, int D)
     }
 }
 
-template <bool WQ, bool EARLY>
+template <bool WQ, bool EARLY, int MAXD>
 int launch_mid(const NodeLaunch &a, int deg, cudaStream_t s) {
-    const size_t smem = (size_t)kMidWarps * kMidMaxDeg * 32 * sizeof(double);
-    auto kern = k_var_mid<WQ, EARLY>;
+    constexpr int kMidWarps = mid_warps<MAXD>();
+    const size_t smem = (size_t)kMidWarps * MAXD * 32 * sizeof(double);
+    auto kern = k_var_mid<WQ, EARLY, MAXD>;
     static bool attr[64] = {};  // the shared-memory attribute is per device
     int dev = 0;
     LDPC_CUDA_TRY(cudaGetDevice(&dev));
@@ -133,11 +145,18 @@ int launch_mid(const NodeLaunch &a, int deg, cudaStream_t s) {
 
 }  // namespace
 
+template <int MAXD>
+int launch_mid_d(const NodeLaunch &a, int deg, bool write_q, cudaStream_t s) {
+    if (a.done != nullptr)
+        return write_q ? launch_mid<true, true, MAXD>(a, deg, s) : launch_mid<false, true, MAXD>(a, deg, s);
+    return write_q ? launch_mid<true, false, MAXD>(a, deg, s) : launch_mid<false, false, MAXD>(a, deg, s);
+}
+
 int launch_var_mid(const NodeLaunch &a, int deg, bool write_q, cudaStream_t s) {
-    LDPC_ARG_CHECK(deg > 0 && deg <= kMidMaxDeg, "mid-degree variable kernel takes degrees up to %d", kMidMaxDeg);
+    LDPC_ARG_CHECK(deg > 0 && deg <= kMaxMidVarDegree, "mid-degree variable kernel takes degrees up to %d",
+                   kMaxMidVarDegree);
     if (a.node_count == 0) return LDPC_OK;
-    if (a.done != nullptr) return write_q ? launch_mid<true, true>(a, deg, s) : launch_mid<false, true>(a, deg, s);
-    return write_q ? launch_mid<true, false>(a, deg, s) : launch_mid<false, false>(a, deg, s);
+    return deg <= 32 ? launch_mid_d<32>(a, deg, write_q, s) : launch_mid_d<64>(a, deg, write_q, s);
 }
 
 }  // namespace ldpc
