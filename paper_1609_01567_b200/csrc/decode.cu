@@ -55,7 +55,7 @@ size_t chain_scratch_doubles(const ldpc_graph *g, int32_t Bp) {
     // per phase: every wide node of the side x its tile x the side's max degree (x2 for r and 1-r)
     size_t wide_c = 0, wide_v = 0;
     for (const Bucket &b : g->chk_buckets)
-        if (b.deg > kMaxRegCheckDegree) wide_c += (size_t)b.node_count;
+        if (b.deg > kMaxMidCheckDegree) wide_c += (size_t)b.node_count;
     for (const Bucket &b : g->var_buckets)
         if (b.deg > kMaxMidVarDegree) wide_v += (size_t)b.node_count;
     size_t need = 0;
@@ -232,13 +232,14 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
     for (const Bucket &b : g->chk_buckets) {
-        if (b.deg <= kMaxRegCheckDegree) {
+        if (b.deg <= kMaxMidCheckDegree) {
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
             a.reverse = alt_sweep() ? ((g_sweep ^= 1) ^ 1) : 0;
-            int rc = use_ring(false, b.deg) ? launch_check_pipe(a, b.deg, from_prior, s)
-                                        : launch_check_bucket(a, b.deg, from_prior, s);
+            int rc = b.deg > kMaxRegCheckDegree ? launch_check_mid(a, b.deg, from_prior, s)
+                     : use_ring(false, b.deg)   ? launch_check_pipe(a, b.deg, from_prior, s)
+                                                : launch_check_bucket(a, b.deg, from_prior, s);
             if (rc) return rc;
         } else {
             if (wide_begin < 0) wide_begin = b.node_begin;

@@ -244,6 +244,7 @@ def test_engine_shared_state_phases(cuda):
     ({90: 8, 300: 2}, {17: 30, 33: 10, 120: 3}, 36),       # small chains blocks, both sides
     ({}, {20: 20, 24: 20, 30: 10, 32: 5}, 70),              # variable degrees 17-32: kernels_varmid.cu
     ({}, {40: 10, 48: 6, 64: 4, 65: 2}, 40),                # 33-64 (4-warp blocks), 65: chains
+    ({48: 12, 64: 8, 65: 2}, {}, 38),                       # checks 33-64 (kernels_varmid.cu), 65: chains
 ])
 def test_mid_degrees_vs_oracle(cuda, check_degrees, extra_vars, B):
     # DVB-S2's high-rate codes have check degrees 18-30 (rates 4/5 .. 9/10)

@@ -15,7 +15,9 @@ from paper_1609_01567_b200 import CodeTables, ParallelDecoder, generate_irregula
 from paper_1609_01567_b200.decoder import priors_awgn_batch  # noqa: E402
 
 B, I = 1024, 10
-H = generate_irregular_code({4: 5832, 3: 52488, 2: 6480}, 6480, seed=910)
+# default: DVB-S2 rate-9/10 shape (check degrees 29/30); --deg40: rate ~0.93 (check degrees 39/40)
+H = (generate_irregular_code({3: 60000, 2: 4800}, 4800, seed=940) if "--deg40" in sys.argv
+     else generate_irregular_code({4: 5832, 3: 52488, 2: 6480}, 6480, seed=910))
 n, m, E = H.n, H.m, H.total_edges
 dc = H.degrees()[1]
 s2 = 1.0 / (2 * 0.9 * 10 ** (4.0 / 10))

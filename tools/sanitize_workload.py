@@ -65,7 +65,8 @@ Pd = torch.empty_like(Yd)
 _native.check(_native.lib().ldpc_priors_awgn(Yd.data_ptr(), Sd.data_ptr(), 8, H1.n, Pd.data_ptr(), None), "priors")
 _native.check(_native.lib().ldpc_npexp(Yd.data_ptr(), Yd.numel(), Pd.data_ptr(), None), "npexp")
 # variables of degree 17-64 (kernels_varmid.cu), early and fixed
-H7 = generate_irregular_code({48: 3, 24: 6, 30: 4, 8: 200, 3: 300, 2: 600}, 420, seed=11)
+H7 = generate_irregular_code({48: 3, 24: 6, 30: 4, 8: 200, 3: 300, 2: 600}, 420, seed=11,
+                             check_degrees={40: 4, 64: 2})
 with ParallelDecoder(CodeTables.from_matrix(H7), max_batch=40) as dec:
     P7 = priors(H7, 40, 1.5, 12)
     dec.decode_priors(P7, 3, early_stop=True, schedule="stream")
