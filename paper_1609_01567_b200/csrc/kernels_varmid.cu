@@ -20,7 +20,8 @@
 namespace ldpc {
 namespace {
 
-constexpr int kMidG = 8;  // outputs per group (chains per lane)
+constexpr int kMidG = 8;    // outputs per group (chains per lane), variables
+constexpr int kMidGC = 16;  // checks (one chain per output: twice the outputs for the same registers)
 // per-warp stage of MAXD rows x 256 bytes; 8 warps per block up to degree 32 (64 KB), 4 past it
 template <int MAXD>
 constexpr int mid_warps() { return MAXD <= 32 ? 8 : 4; }
@@ -164,17 +165,17 @@ __global__ void __launch_bounds__(128) k_check_mid(NodeLaunch a, int D) {
     for (int i = 0; i < D; i++) col[i * 32] = __dsub_rn(1.0, __dmul_rn(2.0, col[i * 32]));
     double *mb = chunk_base(a.msg, a.msg_rows, cw0) + lane;
     double pre = 1.0;
-    for (int k0 = 0; k0 < D; k0 += kMidG) {
-        double acc[kMidG];
+    for (int k0 = 0; k0 < D; k0 += kMidGC) {
+        double acc[kMidGC];
         double q = pre;
 #pragma unroll
-        for (int j = 0; j < kMidG; j++) {
+        for (int j = 0; j < kMidGC; j++) {
             acc[j] = q;
             if (k0 + j < D) q = __dmul_rn(q, col[(k0 + j) * 32]);
         }
         pre = q;
 #pragma unroll
-        for (int jj = 1; jj < kMidG; jj++) {
+        for (int jj = 1; jj < kMidGC; jj++) {
             if (k0 + jj < D) {
                 const double x = col[(k0 + jj) * 32];
 #pragma unroll
@@ -182,13 +183,13 @@ __global__ void __launch_bounds__(128) k_check_mid(NodeLaunch a, int D) {
             }
         }
 #pragma unroll 4
-        for (int i = k0 + kMidG; i < D; i++) {
+        for (int i = k0 + kMidGC; i < D; i++) {
             const double x = col[i * 32];
 #pragma unroll
-            for (int j = 0; j < kMidG; j++) acc[j] = __dmul_rn(acc[j], x);
+            for (int j = 0; j < kMidGC; j++) acc[j] = __dmul_rn(acc[j], x);
         }
 #pragma unroll
-        for (int j = 0; j < kMidG; j++) {
+        for (int j = 0; j < kMidGC; j++) {
             const int k = k0 + j;
             const int slot = pick(id0, id1, k < D ? k : 0);
             if (k < D) st_msg(mb + row_off(slot), __dsub_rn(1.0, __dadd_rn(0.5, __dmul_rn(0.5, acc[j]))));
