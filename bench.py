@@ -121,6 +121,9 @@ def cpu_reference_rate(H, P, iters, seconds):
     return frames * H.n / secs / 1e9, cores, frames, secs
 
 
+PARALLELISM = "dp%d: independent codeword shards, NCCL allreduce of error counts"
+
+
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
@@ -152,7 +155,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: all-zero codeword, BPSK/AWGN at %.1f dB, seeded numpy normals" % args.ebno,
-        "config": workload_desc(cfg, H, B, iters, args.ebno),
+        "config": dict(workload_desc(cfg, H, B, iters, args.ebno), parallelism=PARALLELISM % world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"each step {len(P)} frames of the workload's code (fixed {iters} iterations) "
                                    f"decoded by the C restatement of the reference decoder (oracle/) on "
@@ -486,8 +489,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: all-zero codeword, BPSK/AWGN at %.1f dB, seeded numpy normals; priors by the "
                     "reference's numpy expression" % args.ebno,
-            "config": dict(workload_desc(cfg, H, B, iters, args.ebno),
-                           parallelism=f"dp{world}: independent codeword shards, NCCL allreduce of error counts"),
+            "config": dict(workload_desc(cfg, H, B, iters, args.ebno), parallelism=PARALLELISM % world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(dom), "kernel": dom,
                          "algorithmic_bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_ms,
