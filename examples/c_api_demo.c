@@ -1,12 +1,15 @@
 /*
  * c_api_demo.c -- the C ABI (include/ldpc_b200.h) driven from plain C, no Python or torch:
  * the paper's (14,7) tutorial code (Table I), priors computed the way serial.py:39-50 does,
- * one batch decoded through the host-buffer decoder, results printed.
+ * one batch decoded through the host-buffer decoder, results printed; then the same frames from
+ * their observations y (ldpc_decoder_decode_awgn_host: priors formed on the device with numpy's
+ * exp algorithm).
  *
  *   make -C examples            # gcc, links paper_1609_01567_b200/_native/libldpc_b200.so
  *   ./examples/c_api_demo       # needs a GPU
  *
- * Output: one line per frame "frame k: success=S iterations=I estimate=<14 bits>".
+ * Output: one line per frame "frame k: success=S iterations=I estimate=<14 bits>", then the same
+ * for the observation-input decode, prefixed "obs ".
  */
 #include <math.h>
 #include <stdint.h>
@@ -54,6 +57,16 @@ int main(void) {
           "ldpc_decoder_decode_host");
     for (int f = 0; f < FRAMES; f++) {
         printf("frame %d: success=%d iterations=%d estimate=", f, success[f], iters[f]);
+        for (int j = 0; j < N; j++) putchar('0' + (int)((est[f][j >> 5] >> (j & 31)) & 1u));
+        putchar('\n');
+    }
+    double s2[FRAMES];
+    for (int f = 0; f < FRAMES; f++) s2[f] = sigma2;
+    check(ldpc_decoder_decode_awgn_host(d, &y[0][0], s2, FRAMES, 50, LDPC_FLAG_EARLY_STOP, &est[0][0], success, iters,
+                                        &syn[0][0]),
+          "ldpc_decoder_decode_awgn_host");
+    for (int f = 0; f < FRAMES; f++) {
+        printf("obs frame %d: success=%d iterations=%d estimate=", f, success[f], iters[f]);
         for (int j = 0; j < N; j++) putchar('0' + (int)((est[f][j >> 5] >> (j & 31)) & 1u));
         putchar('\n');
     }

@@ -82,6 +82,16 @@ def test_plain_c_client_matches_python(cuda, tmp_path):
                                           / sigma2)) for j in range(14)] for f in range(3)])
     with ParallelDecoder(CodeTables.from_matrix(ParityCheckMatrix(14, 7, PAIRS_14_7)), max_batch=3) as dec:
         res = dec.decode_priors(P, 50)
-    for f, line in enumerate(lines):
+    assert len(lines) == 6
+    for f, line in enumerate(lines[:3]):
         bits = "".join(str(int(b)) for b in res.estimates()[f])
         assert line == f"frame {f}: success={int(res.success[f])} iterations={int(res.iterations[f])} estimate={bits}"
+    # observation input through the C ABI equals the Python decode_batch(Y, sigma2)
+    Y = np.array([[-1.0 + (1.6 if j in (f, f + 5) else 0.1 * ((j * 7 + f) % 5 - 2)) for j in range(14)]
+                  for f in range(3)])
+    with ParallelDecoder(CodeTables.from_matrix(ParityCheckMatrix(14, 7, PAIRS_14_7)), max_batch=3) as dec:
+        obs = dec.decode_batch(Y, sigma2, 50)
+    for f, line in enumerate(lines[3:]):
+        bits = "".join(str(int(b)) for b in obs.estimates()[f])
+        assert line == (f"obs frame {f}: success={int(obs.success[f])} iterations={int(obs.iterations[f])} "
+                        f"estimate={bits}")
