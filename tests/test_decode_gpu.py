@@ -80,6 +80,8 @@ def test_single_frame_api_matches_golden(cuda, golden_tables, golden_decode):
     ("C2", 40, 1.5, 20, False),
     ("C4", 24, 2.0, 20, True),
     ("C4", 20, 1.0, 8, False),
+    ("C2", 300, 1.5, 20, True),   # B >= 128, early stop: positions in difficulty order
+    ("C1", 1000, 1.0, 30, True),
 ])
 def test_batches_vs_oracle(cuda, code, B, ebno, iters, early):
     from oracle import OracleTables
