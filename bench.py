@@ -102,7 +102,12 @@ def cpu_model() -> str:
 
 
 def cpu_reference_rate(H, P, iters, seconds):
-    """Time the oracle (C restatement of serial.py) on host threads: (Gbit/s, cores, frames, secs)."""
+    """Time the oracle (C restatement of serial.py) on host threads over the workload's frames.
+
+    Decodes every frame of P when that fits ~2x the time budget (it does at C3 on the GPU box's
+    16 threads: 1024 frames in ~2 s), else a bounded prefix of it.  Returns (Gbit/s, cores, frames,
+    secs, outputs) with outputs = (estimate [F, n] u8, success [F] bool, iterations [F] i32,
+    syndrome [F, m] u8) of frames P[:F], the checker for the timed GPU run (parity)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     from oracle import OracleTables  # noqa: E402  (checker / CPU baseline only)
 
@@ -111,14 +116,37 @@ def cpu_reference_rate(H, P, iters, seconds):
     t = time.perf_counter()
     O.decode_batch(P[:1], iters, fixed_iterations=True, n_threads=1)
     per_frame = time.perf_counter() - t
-    frames = int(max(cores, min(len(P), round(seconds * cores / max(per_frame, 1e-3)))))
-    frames = max(cores, (frames // cores) * cores)
-    idx = np.arange(frames) % len(P)
-    Ps = np.ascontiguousarray(P[idx])
+    budget = int(2 * seconds * cores / max(per_frame, 1e-3))
+    frames = len(P) if budget >= len(P) else max(cores, (budget // cores) * cores)
+    Ps = np.ascontiguousarray(P[:frames])
     t = time.perf_counter()
-    O.decode_batch(Ps, iters, fixed_iterations=True, n_threads=cores)
+    outs = O.decode_batch(Ps, iters, fixed_iterations=True, n_threads=cores)
     secs = time.perf_counter() - t
-    return frames * H.n / secs / 1e9, cores, frames, secs
+    return frames * H.n / secs / 1e9, cores, frames, secs, outs
+
+
+def parity_vs_oracle(outs_dev, ref, n, m):
+    """Compare the timed GPU run's outputs (device tensors) with the oracle's on the same frames."""
+    from paper_1609_01567_b200 import unpack_bits
+
+    est_o, ok_o, its_o, z_o = ref
+    F = len(ok_o)
+    est, ok, its, syn = (t[:F].cpu().numpy() for t in outs_dev)
+    bad_est = ~(unpack_bits(est.view(np.uint32), n) == est_o).all(axis=1)
+    bad_ok = ok.astype(bool) != ok_o.astype(bool)
+    bad_its = its != its_o
+    bad_syn = ~(unpack_bits(syn.view(np.uint32), m) == z_o).all(axis=1)
+    bad = bad_est | bad_ok | bad_its | bad_syn
+    return {"frames": int(F), "mismatches": int(bad.sum()),
+            "fields": {"estimate": int(bad_est.sum()), "success": int(bad_ok.sum()),
+                       "iterations": int(bad_its.sum()), "syndrome": int(bad_syn.sum())},
+            "checked": "outputs of the last timed decode_device step vs the C oracle (oracle/) on the same "
+                       "priors: estimate bits, success, iterations, syndrome bits; bit-exact"}
+
+
+def survey_bytes_per_codeword(E, n, iters, w=8):
+    """w*E*(4I+2) + w*n*(I+2) + (n/8)*(2I+2) algorithmic HBM bytes per codeword."""
+    return w * E * (4 * iters + 2) + w * n * (iters + 2) + (n / 8) * (2 * iters + 2)
 
 
 PARALLELISM = "dp%d: independent codeword shards, NCCL allreduce of error counts"
@@ -140,7 +168,9 @@ def run_reference(args):
 
     O = OracleTables.from_matrix(H)
     cores = os.cpu_count() or 1
-    P, _ = synthetic_priors(H, 2 * cores, args.ebno, seed=7)
+    # 64 frames per thread per step: long enough that thread start-up and the tail of the last
+    # frames do not understate the CPU (2 frames per thread read ~15% low in round 1)
+    P, _ = synthetic_priors(H, 64 * cores, args.ebno, seed=7)
     times = []
     for step in range(args.warmup + args.steps):
         t = time.perf_counter()
@@ -157,12 +187,59 @@ def run_reference(args):
         "data": "synthetic: all-zero codeword, BPSK/AWGN at %.1f dB, seeded numpy normals" % args.ebno,
         "config": dict(workload_desc(cfg, H, B, iters, args.ebno), parallelism=PARALLELISM % world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"each step {len(P)} frames of the workload's code (fixed {iters} iterations) "
-                                   f"decoded by the C restatement of the reference decoder (oracle/) on "
-                                   f"{cores} host threads ({cpu_model()})"},
+                         "sample": f"each step {len(P)} frames ({len(P) // cores} per thread) of the workload's "
+                                   f"code (fixed {iters} iterations) decoded by the C restatement of the reference "
+                                   f"decoder (oracle/) on {cores} host threads ({cpu_model()})",
+                         "note": "a C port of the reference's serial.py, ~20x faster per core than the reference's "
+                                 "own numpy ParallelDecoder (see python_engine)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "python_engine": reference_python_engine(H, iters, args.ebno),
     }
     print(json.dumps(line), flush=True)
+
+
+def _py_engine_worker(args):
+    """One process: the reference's own ParallelDecoder (baseline/_ref, unmodified) on frames of H."""
+    path, n, m, rows, cols, Y, s2, iters = args
+    sys.path.insert(0, path)
+    import edgeldpc
+    from edgeldpc.engine import ParallelDecoder as RefDecoder
+
+    Href = edgeldpc.ParityCheckMatrix(n, m, tuple(zip(rows.tolist(), cols.tolist())))
+    T = edgeldpc.CodeTables.from_matrix(Href)
+    dec = RefDecoder(T, 512, n_threads=1)
+    t = time.perf_counter()
+    its = [dec.decode(y, s2, iters).iterations_used for y in Y]
+    return time.perf_counter() - t, its
+
+
+def reference_python_engine(H, iters, ebno, frames_per_core=1):
+    """Context only: the reference's own numpy engine, unmodified, from
+    baseline/_ref (pip --target install of /root/reference), one frame per host core in a process pool.
+    None when the install is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "edgeldpc").is_dir():
+        return None
+    from concurrent.futures import ProcessPoolExecutor
+
+    cores = os.cpu_count() or 1
+    Y, s2 = synthetic_observations(H, cores * frames_per_core, ebno, seed=11)
+    chunks = [Y[i::cores] for i in range(cores)]
+    t = time.perf_counter()
+    try:
+        with ProcessPoolExecutor(cores) as ex:
+            per = list(ex.map(_py_engine_worker,
+                              [(str(ref), H.n, H.m, H.rows, H.cols, c, s2, iters) for c in chunks]))
+    except Exception as e:  # context figure only; never fails the arm
+        return {"error": repr(e)[:200]}
+    wall = time.perf_counter() - t
+    busy = max(p[0] for p in per)
+    its = [i for p in per for i in p[1]]
+    return {"value": len(Y) * H.n / busy / 1e9, "unit": UNIT, "cores": cores, "frames": len(Y),
+            "mean_iterations": float(np.mean(its)),
+            "seconds_decode_max_worker": busy, "seconds_wall_incl_table_build": wall,
+            "path": "baseline/_ref edgeldpc.engine.ParallelDecoder(tables, 512, n_threads=1).decode, one process "
+                    "per core (context for the port's speed; not the reference arm's value)"}
 
 
 # ---- clocks sampler ---------------------------------------------------------------
@@ -295,6 +372,7 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = L.ldpc_kernel_launches() - launches0
+    timed_outs = tuple(t.clone() for t in outs)  # the last timed step's results (checked below)
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -322,7 +400,11 @@ def run_ours(args):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
     step_ms_prof = sum(v["ms"] for v in pd.values()) / args.steps
-    algo_bytes_step = sum(v["bytes"] for v in pd.values()) / args.steps
+    # step level with SURVEY.md 8(d)'s formula (layout passes and the transpose not counted)
+    survey_bpc = survey_bytes_per_codeword(H.total_edges, H.n, iters)
+    step_survey_GBps = B * survey_bpc / (ms_step / 1e3) / 1e9
+    class_frac = {k: (v["bytes"] / (v["ms"] / 1e3) / 1e9) / peak for k, v in pd.items()
+                  if k in ("check", "variable", "estimate") and v["ms"] > 0}
 
     # e2e through the public host API: pinned priors in, packed results out, every step
     e2e = e2e_stream = e2e_from_y = None
@@ -475,12 +557,13 @@ def run_ours(args):
                                      "path": "ParallelDecoder.decode(y, sigma2): H2D of y, device prior, "
                                              "grid schedule (one cooperative launch), D2H"}
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cores, frames, secs = cpu_reference_rate(H, P_host, iters, args.cpu_seconds)
+        v, cores, frames, secs, ref_outs = cpu_reference_rate(H, P_host, iters, args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{frames} frames of the workload (fixed {iters} iterations) in {secs:.1f} s by the C "
                          f"restatement of the reference decoder (oracle/) on {cores} host threads ({cpu_model()})"}
+        parity = parity_vs_oracle(timed_outs, ref_outs, H.n, H.m)
 
     if rank == 0:
         line = {
@@ -494,8 +577,13 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": load_traffic(dom), "kernel": dom,
                          "algorithmic_bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6.65 TB/s",
-                         "step_algorithmic_GBps": algo_bytes_step / (step_ms_prof / 1e3) / 1e9,
+                         "step": {"bytes_per_codeword": survey_bpc, "GBps": step_survey_GBps,
+                                  "frac": step_survey_GBps / peak,
+                                  "formula": "SURVEY.md 8(d): 8*E*(4I+2) + 8*n*(I+2) + (n/8)*(2I+2) per codeword "
+                                             "/ device-timed ms_per_step"},
+                         "class_frac": class_frac,
                          "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in pd.items()}},
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_stream": e2e_stream,
@@ -511,6 +599,9 @@ def run_ours(args):
     dec.close()
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and parity["mismatches"]:
+        sys.stderr.write(f"PARITY FAILURE: {parity['mismatches']} of {parity['frames']} frames differ from the oracle\n")
+        sys.exit(3)
 
 
 def main():

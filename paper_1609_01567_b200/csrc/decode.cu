@@ -477,18 +477,35 @@ static int decode_impl(const ldpc_graph *g, const double *p_dev, const double *s
                                        syn_bits_dev, workspace_dev, stream};
         std::shared_ptr<ldpc_graph::GraphEntry> entry;
         bool capture = false;
+        cudaGraphExec_t exec_now = nullptr;
+        long long exec_kernels = 0;
         {
             std::lock_guard<std::mutex> lock(gg->graphs_mu);
             auto it = gg->graphs.find(key);
             if (it == gg->graphs.end()) {
-                if (gg->graphs.size() >= kMaxGraphKeys)  // bounded: drop keys that never repeated
+                if (gg->graphs.size() >= kMaxGraphKeys) {
+                    // bounded: drop keys that never repeated, then the least recently used captured
+                    // ones (an evicted entry a caller still holds lives on through its shared_ptr)
                     for (auto e = gg->graphs.begin(); e != gg->graphs.end();)
                         e = (e->second->exec == nullptr && !e->second->capturing) ? gg->graphs.erase(e) : std::next(e);
+                    while (gg->graphs.size() >= kMaxGraphKeys) {
+                        auto lru = gg->graphs.end();
+                        for (auto e = gg->graphs.begin(); e != gg->graphs.end(); ++e)
+                            if (!e->second->capturing && (lru == gg->graphs.end() ||
+                                                          e->second->last_use < lru->second->last_use))
+                                lru = e;
+                        if (lru == gg->graphs.end()) break;
+                        gg->graphs.erase(lru);
+                    }
+                }
                 it = gg->graphs.emplace(key, std::make_shared<ldpc_graph::GraphEntry>()).first;
             }
             entry = it->second;
             entry->uses++;
+            entry->last_use = ++gg->graph_clock;
             if (entry->exec == nullptr && !entry->capturing && entry->uses >= 2) capture = entry->capturing = true;
+            exec_now = entry->exec;
+            exec_kernels = entry->kernels;
         }
         if (capture) {
             cudaGraph_t graph = nullptr;
@@ -518,10 +535,12 @@ static int decode_impl(const ldpc_graph *g, const double *p_dev, const double *s
                 set_error("graph capture: %s", cudaGetErrorString(ce));
                 return LDPC_ECUDA;
             }
+            exec_now = exec;
+            exec_kernels = kernels;
         }
-        if (entry->exec != nullptr) {
-            LDPC_CUDA_TRY(cudaGraphLaunch(entry->exec, s));
-            count_launches(entry->kernels);
+        if (exec_now != nullptr) {  // entry (held above) keeps exec_now alive through the launch
+            LDPC_CUDA_TRY(cudaGraphLaunch(exec_now, s));
+            count_launches(exec_kernels);
             return LDPC_OK;
         }
     }
@@ -808,9 +827,12 @@ extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32
     d->g = g;
     d->max_batch = max_batch;
     d->sub = sub_batch > 0 ? std::min(sub_batch, max_batch) : std::min(max_batch, 512);
-    // the largest sub-batch the plan can produce (the last chunk may absorb a remainder)
+    // the largest sub-batch the plan produces for ANY batch the decoder accepts: a smaller batch
+    // can merge its remainder into a larger last chunk than max_batch's plan has (e.g. B = 800 with
+    // sub = 512: 64, 128, 192, 416), so take the maximum over every b <= max_batch
     int32_t biggest = 0;
-    for (int32_t b : chunk_plan(max_batch, d->sub)) biggest = std::max(biggest, b);
+    for (int32_t b = max_batch; b >= 1 && biggest < max_batch; b--)
+        for (int32_t x : chunk_plan(b, d->sub)) biggest = std::max(biggest, x);
     d->ws_bytes = workspace_bytes(g, biggest);
     const size_t RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32, MB = (size_t)max_batch;
     cudaError_t e = cudaSuccess;

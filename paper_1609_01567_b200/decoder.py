@@ -473,7 +473,8 @@ class ParallelDecoder:
                                             ctypes.byref(h)), "ldpc_decoder_create")
         self._h = h
         self._closed = False
-        self._lock = threading.Lock()
+        self._pinned = None
+        self._lock = threading.RLock()
 
     # engine.py:363-398
     def decode(self, y, sigma2: float, max_iterations: int = DEFAULT_MAX_ITERATIONS) -> DecodeResult:
@@ -514,18 +515,22 @@ class ParallelDecoder:
                              precision, schedule)
         res = out if out is not None else BatchResult(np.empty((B, (n + 31) // 32), np.uint32), np.empty(B, np.uint8), np.empty(B, np.int32),
                           np.empty((B, (m + 31) // 32), np.uint32), n, m)
-        # priors go into a reused pinned buffer (no page faults, full-speed copies), max_batch frames at a time
-        buf = self._pinned_priors()
-        for c0 in range(0, B, self.max_batch):
-            c1 = min(B, c0 + self.max_batch)
-            P = priors_awgn_batch(Y[c0:c1], s2[c0:c1], out=buf[:c1 - c0])
-            self.decode_priors(P, max_iterations, early_stop, precision=precision, schedule=schedule,
-                               out=BatchResult(res.est_bits[c0:c1], res.success[c0:c1], res.iterations[c0:c1],
-                                               res.syn_bits[c0:c1], n, m))
+        # priors go into a reused pinned buffer (no page faults, full-speed copies), max_batch frames at a
+        # time; the buffer is shared by the instance, so concurrent calls hold the (reentrant) lock across
+        # forming the priors and decoding them
+        with self._lock:
+            buf = self._pinned_priors()
+            for c0 in range(0, B, self.max_batch):
+                c1 = min(B, c0 + self.max_batch)
+                P = priors_awgn_batch(Y[c0:c1], s2[c0:c1], out=buf[:c1 - c0])
+                self.decode_priors(P, max_iterations, early_stop, precision=precision, schedule=schedule,
+                                   out=BatchResult(res.est_bits[c0:c1], res.success[c0:c1], res.iterations[c0:c1],
+                                                   res.syn_bits[c0:c1], n, m))
         return res
 
     def _pinned_priors(self) -> np.ndarray:
-        if getattr(self, "_pinned", None) is None:
+        """The instance's pinned [max_batch, n] priors buffer (caller holds self._lock)."""
+        if self._pinned is None:
             torch = _torch()
             self._pinned = torch.empty((self.max_batch, self.tables.n), dtype=torch.float64).pin_memory().numpy()
         return self._pinned

@@ -96,48 +96,81 @@ class DeviceGraph:
 class CodeTables:
     """Both orientations plus node/edge counts (tables.py:95-116), device-resident.
 
-    ``variable``/``check``/``var_group_start``/``var_group_size`` are the
-    reference's host arrays, exported from the device graph on first access.
+    Constructible like the reference's frozen dataclass from its seven fields
+    ``CodeTables(variable, check, n, m, total_edges, var_group_start,
+    var_group_size)``; the device graph is then built on first use from the
+    variable-oriented (c, v) pairs.  ``from_matrix`` builds the device graph
+    first (G1 builder) and exports the reference's host arrays lazily.
+    Immutable: attribute assignment raises, like the reference's.
     """
 
-    def __init__(self, graph: DeviceGraph, H: ParityCheckMatrix | None = None):
-        self.graph = graph
-        self.H = H
-        self.n, self.m, self.total_edges = graph.n, graph.m, graph.E
-        self._var = self._chk = None
-        self._groups = None
+    def __init__(self, variable: EdgeTables, check: EdgeTables, n: int, m: int, total_edges: int,
+                 var_group_start: np.ndarray, var_group_size: np.ndarray):
+        if variable.orientation != VARIABLE or check.orientation != CHECK:
+            raise ValueError("expected variable- and check-oriented edge tables")
+        self._set(_graph=None, _var=variable, _chk=check, _groups=(var_group_start, var_group_size),
+                  n=int(n), m=int(m), total_edges=int(total_edges))
+
+    def _set(self, **kw):
+        for k, v in kw.items():
+            object.__setattr__(self, k, v)
+
+    def __setattr__(self, name, value):
+        raise AttributeError(f"cannot assign to field {name!r}: CodeTables is immutable")
+
+    @classmethod
+    def _of_graph(cls, graph: DeviceGraph) -> "CodeTables":
+        self = cls.__new__(cls)
+        self._set(_graph=graph, _var=None, _chk=None, _groups=None, n=graph.n, m=graph.m, total_edges=graph.E)
+        return self
 
     @classmethod
     def from_matrix(cls, H: ParityCheckMatrix) -> "CodeTables":
-        return cls(DeviceGraph(H), H)
+        # no back-reference to H: a matrix-keyed cache of tables must not keep its key alive
+        return cls._of_graph(DeviceGraph(H))
+
+    @property
+    def graph(self) -> DeviceGraph:
+        """The device graph (G1), built from the variable tables' (c, v) pairs when the tables
+        were constructed field by field."""
+        if self._graph is None:
+            v = self._var
+            H = ParityCheckMatrix(self.n, self.m, np.stack([np.asarray(v.c), np.asarray(v.v)], axis=1))
+            if H.total_edges != self.total_edges:
+                raise ValueError("total_edges does not match the edge tables")
+            self._set(_graph=DeviceGraph(H))
+        return self._graph
 
     @property
     def variable(self) -> EdgeTables:
         if self._var is None:
-            self._var = self.graph.export(VARIABLE)
+            self._set(_var=self._graph.export(VARIABLE))
         return self._var
 
     @property
     def check(self) -> EdgeTables:
         if self._chk is None:
-            self._chk = self.graph.export(CHECK)
+            self._set(_chk=self._graph.export(CHECK))
         return self._chk
 
     @property
     def var_group_start(self) -> np.ndarray:
         if self._groups is None:
-            self._groups = self.graph.var_groups()
+            self._set(_groups=self._graph.var_groups())
         return self._groups[0]
 
     @property
     def var_group_size(self) -> np.ndarray:
         if self._groups is None:
-            self._groups = self.graph.var_groups()
+            self._set(_groups=self._graph.var_groups())
         return self._groups[1]
 
     def buckets(self, side: str = VARIABLE) -> list[tuple[int, int]]:
         """Degree buckets [(degree, node count)] of one side, ascending degree."""
         return self.graph.buckets(side)
+
+    def __repr__(self) -> str:
+        return f"CodeTables(n={self.n}, m={self.m}, total_edges={self.total_edges})"
 
 
 def build_variable_tables(H: ParityCheckMatrix) -> EdgeTables:

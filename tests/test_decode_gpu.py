@@ -284,3 +284,52 @@ def test_batches_larger_than_max_batch_are_pipelined(cuda):
             assert np.array_equal(a.success, b.success) and np.array_equal(a.iterations, b.iterations)
     est, ok, its, z = OracleTables.from_matrix(H).decode_batch(P, 30, fixed_iterations=True)
     assert np.array_equal(a.estimates(), est) and np.array_equal(a.iterations, its)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("mode", ["fixed", "early"])
+def test_c3_full_batch_timed_path_all_frames(cuda, mode):
+    """The bench's timed path at its full size: C3, B = 1024, one decode_device call (whole batch,
+    CUDA-graph replay on the third call), every frame bit-exact vs the oracle (serial.py:150-178,
+    engine.py:363-398).  fixed: the bench workload itself (2 dB, 10 rounds, bench.py's seed);
+    early: 3 dB, 30 rounds, where frames stop at different rounds."""
+    import torch
+
+    from oracle import OracleTables
+    from paper_1609_01567_b200 import unpack_bits
+
+    H = configs.code("C3")
+    ebno, iters, early = (2.0, 10, False) if mode == "fixed" else (3.0, 30, True)
+    s2 = configs.ebno_to_sigma2(ebno, configs.rate(H))
+    rng = np.random.default_rng(1000)
+    P = priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((1024, H.n)), s2)
+    T = CodeTables.from_matrix(H)
+    with ParallelDecoder(T, max_batch=1024) as dec:
+        P_dev = torch.from_numpy(P).cuda()
+        ws, outs = dec.workspace(1024), dec.alloc_outputs(1024, P_dev.device)
+        for _ in range(3):  # eager, capture, replay: the replayed graph is what the bench times
+            dec.decode_device(P_dev, iters, early_stop=early, workspace=ws, outputs=outs)
+        est, ok, its, syn = (t.cpu().numpy() for t in outs)
+    e_o, ok_o, it_o, z_o = OracleTables.from_matrix(H).decode_batch(P, iters, fixed_iterations=not early)
+    assert np.array_equal(unpack_bits(est.view(np.uint32), H.n), e_o)
+    assert np.array_equal(ok.astype(bool), ok_o)
+    assert np.array_equal(its, it_o)
+    assert np.array_equal(unpack_bits(syn.view(np.uint32), H.m), z_o)
+    if early:
+        assert len(np.unique(it_o)) > 3, "early-stop case should spread stopping rounds"
+
+
+@pytest.mark.parametrize("B", [800, 769, 895, 1000])
+def test_host_decoder_any_batch_up_to_max_batch(cuda, B):
+    """chunk_plan(B) for B < max_batch can merge a remainder into a sub-batch larger than
+    max_batch's plan has; the per-lane workspace must cover it (C2, a streaming-schedule code)."""
+    from oracle import OracleTables
+
+    H, P = _frames("C2", B, 1.8, seed=B)
+    with ParallelDecoder(CodeTables.from_matrix(H), max_batch=1024) as dec:
+        res = dec.decode_priors(P, 12, early_stop=True)
+    sample = np.arange(0, B, 41)
+    e, ok, it, z = OracleTables.from_matrix(H).decode_batch(P[sample], 12)
+    assert np.array_equal(res.estimates()[sample], e)
+    assert np.array_equal(res.iterations[sample], it)
+    assert np.array_equal(res.success[sample].astype(bool), ok)

@@ -38,6 +38,70 @@ class TestParityCheckMatrix:
         with pytest.raises(ValueError):
             ParityCheckMatrix(n, m, ones)
 
+    # value semantics of the reference's frozen dataclass (codes.py:29-61)
+    def test_any_iterable_of_pairs(self):
+        pairs = [(1, 2), (0, 0), (0, 1), (1, 1)]
+        ref = ParityCheckMatrix(3, 2, tuple(pairs))
+        assert ParityCheckMatrix(3, 2, set(pairs)) == ref
+        assert ParityCheckMatrix(3, 2, (p for p in pairs)) == ref
+        assert ParityCheckMatrix(3, 2, [list(p) for p in pairs]) == ref
+        assert ParityCheckMatrix(3, 2, np.array(pairs)) == ref
+        assert ParityCheckMatrix(3, 2, [(np.int64(r), float(c)) for r, c in pairs]) == ref
+
+    def test_immutable_and_hashable(self):
+        H = ParityCheckMatrix(14, 7, PAIRS_14_7)
+        H2 = ParityCheckMatrix(14, 7, tuple(reversed(PAIRS_14_7)))
+        assert H == H2 and hash(H) == hash(H2)
+        assert len({H, H2, ParityCheckMatrix(3, 2, ((0, 0), (0, 1), (1, 2)))}) == 2
+        with pytest.raises(AttributeError):
+            H.n = 5
+        with pytest.raises(AttributeError):
+            del H.m
+        with pytest.raises(ValueError):
+            H.rows[0] = 3          # read-only coordinates
+        assert H != "H" and H != ParityCheckMatrix(14, 7, PAIRS_14_7[:-1] + ((6, 13),))
+
+    def test_pickle_round_trip(self):
+        import copy
+        import pickle
+
+        H = ParityCheckMatrix(14, 7, PAIRS_14_7)
+        assert pickle.loads(pickle.dumps(H)) == H
+        assert copy.deepcopy(H) == H
+
+
+def test_code_info_value_type():
+    # codes.py:95-105: frozen dataclass, equal field by field, readable repr
+    from paper_1609_01567_b200 import CodeInfo
+
+    H = ParityCheckMatrix(14, 7, PAIRS_14_7)
+    info = CodeInfo.from_matrix(H)
+    assert info == CodeInfo(31, 14, 7) and hash(info) == hash(CodeInfo(31, 14, 7))
+    assert repr(info) == "CodeInfo(total_edges=31, var_nodes=14, check_nodes=7)"
+    with pytest.raises(AttributeError):
+        info.total_edges = 1
+
+
+def test_code_tables_constructible_from_fields():
+    # tables.py:95-105: CodeTables(variable, check, n, m, total_edges, var_group_start, var_group_size)
+    # without touching the device; immutable
+    from conftest import GOLDEN_CHECK, GOLDEN_VARIABLE
+    from paper_1609_01567_b200 import CodeTables, EdgeTables
+
+    var = EdgeTables("variable", *(np.array(GOLDEN_VARIABLE[k]) for k in "evctsu"))
+    chk = EdgeTables("check", *(np.array(GOLDEN_CHECK[k]) for k in "evctsu"))
+    firsts = var.u == 0
+    gs, gz = np.empty(14, np.int64), np.empty(14, np.int64)
+    gs[var.v[firsts]], gz[var.v[firsts]] = var.s[firsts], var.t[firsts]
+    T = CodeTables(var, chk, 14, 7, 31, gs, gz)
+    assert T.n == 14 and T.m == 7 and T.total_edges == 31
+    assert T.variable is var and T.check is chk
+    assert np.array_equal(T.var_group_size, [4, 2, 2, 3, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2])
+    with pytest.raises(AttributeError):
+        T.n = 3
+    with pytest.raises(ValueError):
+        CodeTables(chk, var, 14, 7, 31, gs, gz)
+
 
 class TestAlist:
     def test_fixture_round_trip(self):
