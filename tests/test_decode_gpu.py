@@ -333,3 +333,24 @@ def test_host_decoder_any_batch_up_to_max_batch(cuda, B):
     assert np.array_equal(res.estimates()[sample], e)
     assert np.array_equal(res.iterations[sample], it)
     assert np.array_equal(res.success[sample].astype(bool), ok)
+
+
+def test_matrix_keyed_device_tables_are_released(cuda):
+    """tables cached for a ParityCheckMatrix passed where the reference takes H
+    (syndrome, decode_awgn) die with the matrix (CodeTables holds no reference back to it)."""
+    import gc
+    import weakref
+
+    from paper_1609_01567_b200 import decoder as D
+
+    base = configs.code("C1")
+    H = ParityCheckMatrix(base.n, base.m, np.stack([base.rows, base.cols], axis=1))
+    z = syndrome(np.zeros(H.n, np.uint8), H)
+    assert not z.any()
+    key = id(H)
+    assert dict.__contains__(D._H_TABLES, key)
+    graph = weakref.ref(dict.__getitem__(D._H_TABLES, key).graph)
+    del H
+    gc.collect()
+    assert not dict.__contains__(D._H_TABLES, key)
+    assert graph() is None
