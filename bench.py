@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-configs", action="store_true", help="skip the other-BASELINE-configs leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--sub-batch", type=int, default=0, help="e2e pipeline sub-batch (0 = decoder default)")
+    ap.add_argument("--seed", type=int, default=1000, help="rank r draws its synthetic frames with seed + r")
     return ap.parse_args()
 
 
@@ -340,19 +341,22 @@ def run_ours(args):
     iters = args.iters if args.iters is not None else C["max_iterations"]
     T = CodeTables.from_matrix(H)
     dec = ParallelDecoder(T, max_batch=B, sub_batch=args.sub_batch)
-    P_host, _ = synthetic_priors(H, B, args.ebno, seed=1000 + rank)
+    P_host, _ = synthetic_priors(H, B, args.ebno, seed=args.seed + rank)
     P_pin = torch.from_numpy(P_host).pin_memory()
     P_dev = P_pin.to(dev, non_blocking=True)
     ws = dec.workspace(B)
     outs = dec.alloc_outputs(B, dev)
-    counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    counts = torch.zeros(4, dtype=torch.int64, device=dev)       # whole run, all ranks
+    step_counts = torch.zeros(4, dtype=torch.int64, device=dev)  # one step, folded over ranks
     stream = torch.cuda.current_stream()
 
     def step(profile=None):
         dec.decode_device(P_dev, iters, early_stop=False, workspace=ws, outputs=outs, profile=profile)
-        dec.count_errors(outs, counts)
+        step_counts.zero_()
+        dec.count_errors(outs, step_counts)
         if world > 1:
-            dist.all_reduce(counts)
+            dist.all_reduce(step_counts)  # the only collective: int64[4] error counters
+        counts.add_(step_counts)
 
     for _ in range(args.warmup):
         step()

@@ -5,7 +5,7 @@ BASELINE.json "configs" (SURVEY.md section 8 shapes):
   C2  n=8192 rate 1/2, batch 4096, 20 iterations
   C3  DVB-S2-shaped n=64800 rate 1/2: 12,960 vars of degree 8, 19,440 of degree 3,
       32,400 of degree 2; check degree 7 (E = 226,800); batch 1024; fixed 10 iterations
-  C4  high-degree stress: n=32768, checks up to degree 1000, vars up to degree 200, early stop
+  C4  high-degree stress: n=32768, checks of degree 20-1000, vars of degree 17-200, early stop (3 dB)
   C5  C3's code, Eb/N0 0..3 dB sweep, sharded over GPUs with an error-count allreduce
 """
 
@@ -34,9 +34,15 @@ def code(name: str) -> ParityCheckMatrix:
         return generate_irregular_code({8: 1638, 3: 2458, 2: 4096}, 4096, seed=SEED + 2)
     if name in ("C3", "C5"):
         return generate_irregular_code({8: 12960, 3: 19440, 2: 32400}, 32400, seed=SEED + 3)
-    if name == "C4":      # 16 checks of degree 1000, 16 vars of degree 200
-        return generate_irregular_code({200: 16, 8: 1024, 3: 15728, 2: 16000}, 16384, seed=SEED + 4,
-                                       check_degrees={1000: 16})
+    if name == "C4":
+        # high degrees spread over the range: checks of degree 20-1000 (452 checks, 24% of the
+        # edges) and variables of degree 17-200 (256 variables, 9% of the edges); the rest are
+        # degree-6 / degree-3 variables and checks of degree 5-6.  No degree-2 variables: with a
+        # quarter of the edges on weak high-degree checks they would leave uncorrectable bits, and
+        # the code must converge (early stop fires at 3 dB: ~70% of frames in 8-20 rounds).
+        return generate_irregular_code({200: 16, 120: 16, 60: 32, 30: 64, 17: 128, 6: 4000, 3: 28512}, 16384,
+                                       seed=SEED + 4,
+                                       check_degrees={1000: 4, 500: 8, 250: 16, 120: 32, 60: 64, 33: 128, 20: 256})
     raise KeyError(name)
 
 
@@ -44,7 +50,7 @@ CONFIGS = {
     "C1": dict(code="C1", batch=1, max_iterations=50, ebno_db=2.0, early_stop=True),
     "C2": dict(code="C2", batch=4096, max_iterations=20, ebno_db=2.0, early_stop=True),
     "C3": dict(code="C3", batch=1024, max_iterations=10, ebno_db=2.0, early_stop=False),
-    "C4": dict(code="C4", batch=256, max_iterations=20, ebno_db=2.0, early_stop=True),
+    "C4": dict(code="C4", batch=256, max_iterations=20, ebno_db=3.0, early_stop=True),
     "C5": dict(code="C5", batch=1024, max_iterations=10, ebno_db=(0.0, 1.0, 2.0, 3.0), early_stop=True),
 }
 

@@ -76,6 +76,7 @@ size_t workspace_bytes(const ldpc_graph *g, int32_t B) {
     b += align256(sizeof(uint32_t) * (size_t)g->m * NW);
     b += align256(sizeof(uint32_t) * NW) * 2;
     b += align256(sizeof(int32_t) * Bp);
+    b += align256(sizeof(float) * (size_t)kOdScratchBlocks * fast_od_scratch_stride(g));
     return b;
 }
 
@@ -105,6 +106,8 @@ int carve_workspace(const ldpc_graph *g, int32_t B, void *ws, size_t bytes, Work
     w->done = (uint32_t *)take(sizeof(uint32_t) * w->NW);
     w->unsat = (uint32_t *)take(sizeof(uint32_t) * w->NW);
     w->iters = (int32_t *)take(sizeof(int32_t) * w->Bp);
+    w->od_stride = fast_od_scratch_stride(g);
+    w->od_scratch = w->od_stride ? (float *)take(sizeof(float) * (size_t)kOdScratchBlocks * w->od_stride) : nullptr;
     return LDPC_OK;
 }
 
@@ -208,6 +211,17 @@ float *prior32(const ldpc_graph *g, const Workspace &w) { return reinterpret_cas
 // kernel before it, so it starts on the chunk whose rows the previous kernel touched last and
 // finds part of them in L2 (C3 step 14.16 -> 14.02 ms with default-caching hints;
 // profiles/r1_kernel_choice.md).  LDPC_ALT_SWEEP=0 disables it.
+// fp32 fast mode: nodes of degree <= kMaxRegDegree take the fp32 register kernels (the reference's
+// product order, kernels_fast.cu); from this degree on the O(d) kernels (kernels_fastod.cu).
+// LDPC_FAST_OD=1 sends every degree to the O(d) kernels.
+static int fast_od_min_degree() {
+    static const int v = [] {
+        const char *e = getenv("LDPC_FAST_OD");
+        return (e && e[0] == '1') ? 1 : kMaxRegDegree + 1;
+    }();
+    return v;
+}
+
 static bool alt_sweep() {
     static const bool on = [] {
         const char *e = getenv("LDPC_ALT_SWEEP");
@@ -222,13 +236,15 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
     NodeLaunch a = check_args(g, w, done);
     if (fast) {
         for (const Bucket &b : g->chk_buckets) {
+            if (b.deg >= fast_od_min_degree()) break;  // buckets are sorted by degree
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
             int rc = launch_check_f32(a, b.deg, from_prior, msg32(g, w), prior32(g, w), s);
             if (rc) return rc;
         }
-        return LDPC_OK;
+        return launch_fast_od(a, g->chk_buckets, fast_od_min_degree(), false, from_prior, msg32(g, w), prior32(g, w),
+                              w.od_scratch, w.od_stride, kOdScratchBlocks, s);
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
     for (const Bucket &b : g->chk_buckets) {
@@ -260,13 +276,15 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
     NodeLaunch a = var_args(g, w, done);
     if (fast) {
         for (const Bucket &b : g->var_buckets) {
+            if (b.deg >= fast_od_min_degree()) break;  // buckets are sorted by degree
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
             int rc = launch_var_f32(a, b.deg, write_q, msg32(g, w), prior32(g, w), s);
             if (rc) return rc;
         }
-        return LDPC_OK;
+        return launch_fast_od(a, g->var_buckets, fast_od_min_degree(), true, write_q, msg32(g, w), nullptr, nullptr, 0,
+                              0, s);
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
     for (const Bucket &b : g->var_buckets) {
@@ -422,8 +440,6 @@ static int decode_impl(const ldpc_graph *g, const double *p_dev, const double *s
                               LDPC_FLAG_GRID)) == 0,
                    "unknown flags 0x%x", flags);
     const bool fast = (flags & LDPC_FLAG_FP32) != 0;
-    LDPC_ARG_CHECK(!fast || (g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree),
-                   "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
     LDPC_ARG_CHECK(__builtin_popcount(flags & (LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP | LDPC_FLAG_GRID)) <= 1,
                    "at most one schedule flag");
     cudaStream_t s = (cudaStream_t)stream;
@@ -579,8 +595,6 @@ extern "C" int ldpc_decode_channel(const ldpc_graph *g, uint64_t seed, uint64_t 
     LDPC_ARG_CHECK((flags & ~(LDPC_FLAG_FIXED_ITERS | LDPC_FLAG_FP32 | LDPC_FLAG_STREAMING | LDPC_FLAG_ONCHIP)) == 0,
                    "unknown flags 0x%x", flags);
     const bool fast = (flags & LDPC_FLAG_FP32) != 0;
-    LDPC_ARG_CHECK(!fast || (g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree),
-                   "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
     cudaStream_t s = (cudaStream_t)stream;
     const bool early = !(flags & LDPC_FLAG_FIXED_ITERS);
     // (device-generated priors land chunk-major, so this path always streams)
@@ -667,8 +681,6 @@ extern "C" int ldpc_phase_f32(const ldpc_graph *g, int phase, const double *p_de
     LDPC_ARG_CHECK(g && in_dev && out_dev && (phase == 1 || p_dev), "NULL argument");
     DeviceGuard dg(g->device);
     LDPC_ARG_CHECK(phase == 0 || phase == 1, "phase must be 0 (to check) or 1 (to variable)");
-    LDPC_ARG_CHECK(g->max_dv <= kMaxRegDegree && g->max_dc <= kMaxRegDegree,
-                   "fp32 fast mode supports node degrees up to %d", kMaxRegDegree);
     Workspace w;
     int rc = carve_workspace(g, B, ws, ws_bytes, &w);
     if (rc) return rc;

@@ -78,7 +78,7 @@ def test_single_frame_api_matches_golden(cuda, golden_tables, golden_decode):
     ("C1", 33, 1.0, 50, True),
     ("C2", 64, 2.0, 20, True),
     ("C2", 40, 1.5, 20, False),
-    ("C4", 24, 2.0, 20, True),
+    ("C4", 24, 3.0, 20, True),
     ("C4", 20, 1.0, 8, False),
     ("C2", 300, 1.5, 20, True),   # B >= 128, early stop: positions in difficulty order
     ("C1", 1000, 1.0, 30, True),

@@ -130,7 +130,10 @@ class TestGenerator:
     def test_high_degree_profile(self):
         H = configs.code("C4")
         dv, dc = H.degrees()
-        assert dv.max() == 200 and dc.max() == 1000 and (dc == 1000).sum() == 16
+        assert dv.max() == 200 and dc.max() == 1000 and (dc == 1000).sum() == 4
+        assert sorted(set(dc[dc > 16].tolist())) == [20, 33, 60, 120, 250, 500, 1000]
+        assert sorted(set(dv[dv > 16].tolist())) == [17, 30, 60, 120, 200]
+        assert H.n == 32768 and H.m == 16384
 
     def test_deterministic(self):
         a = generate_irregular_code({3: 40, 2: 20}, 25, seed=5)

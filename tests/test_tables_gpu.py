@@ -99,7 +99,7 @@ def test_dvbs2_tables_vs_oracle(cuda):
 def test_high_degree_buckets(cuda):
     H = configs.code("C4")
     T = CodeTables.from_matrix(H)
-    assert T.buckets("check")[-1] == (1000, 16)
+    assert T.buckets("check")[-1] == (1000, 4)
     assert T.buckets("variable")[-1] == (200, 16)
     assert T.graph.max_dc == 1000 and T.graph.max_dv == 200
 
