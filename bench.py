@@ -499,7 +499,7 @@ def run_ours(args):
 
     # f4 fast mode (fp32, not bit-exact): same workload, device-timed, agreement with the exact run
     fast = None
-    if not args.no_fast and H.total_edges and max(H.degrees()[0].max(), H.degrees()[1].max()) <= 16:
+    if not args.no_fast:
         outs32 = dec.alloc_outputs(B, dev)
         for _ in range(args.warmup):
             dec.decode_device(P_dev, iters, early_stop=False, workspace=ws, outputs=outs32, precision="fp32")
@@ -521,28 +521,43 @@ def run_ours(args):
     others = None
     if world == 1 and not args.no_configs and cfg == "C3":
         others = {}
-        for name, B_o, it_o, early_o in (("C1", 1, 50, True), ("C2", 4096, 20, False), ("C4", 256, 20, True)):
+        # (label, code, batch, iterations, early stop, Eb/N0, precision); C2/C4 at the config's Eb/N0
+        runs = (("C1", "C1", 1, 50, True, 2.0, "fp64"),
+                ("C2", "C2", 4096, 20, True, 2.0, "fp64"),
+                ("C2_fixed", "C2", 4096, 20, False, 2.0, "fp64"),
+                ("C4", "C4", 256, 20, True, 3.0, "fp64"),
+                ("C4_fast_fp32", "C4", 256, 20, True, 3.0, "fp32"),
+                ("C5_3dB", "C5", 1024, 10, True, 3.0, "fp64"))
+        for label, name, B_o, it_o, early_o, eb_o, prec_o in runs:
             H_o = configs.code(name)
             T_o = CodeTables.from_matrix(H_o)
-            P_o = torch.from_numpy(synthetic_priors(H_o, B_o, args.ebno, seed=5)[0]).to(dev)
+            P_o = torch.from_numpy(synthetic_priors(H_o, B_o, eb_o, seed=5)[0]).to(dev)
             with ParallelDecoder(T_o, max_batch=B_o) as d_o:
                 ws_o, outs_o = d_o.workspace(B_o), d_o.alloc_outputs(B_o, dev)
                 for _ in range(3):
-                    d_o.decode_device(P_o, it_o, early_stop=early_o, workspace=ws_o, outputs=outs_o)
+                    d_o.decode_device(P_o, it_o, early_stop=early_o, workspace=ws_o, outputs=outs_o,
+                                      precision=prec_o)
                 reps = 20 if B_o < 64 else 5
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
                 e0.record(stream)
                 for _ in range(reps):
-                    d_o.decode_device(P_o, it_o, early_stop=early_o, workspace=ws_o, outputs=outs_o)
+                    d_o.decode_device(P_o, it_o, early_stop=early_o, workspace=ws_o, outputs=outs_o,
+                                      precision=prec_o)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 ms_o = e0.elapsed_time(e1) / reps
-                its_o = outs_o[2].float().mean().item()
-            others[name] = {"batch": B_o, "max_iterations": it_o, "early_stop": early_o, "ms_per_decode": ms_o,
-                            "coded_Gbit_s": B_o * H_o.n / (ms_o / 1e3) / 1e9, "mean_iterations": its_o,
-                            "n": H_o.n, "edges": H_o.total_edges}
+                its_o = outs_o[2].float()
+            others[label] = {"batch": B_o, "max_iterations": it_o, "early_stop": early_o, "ebno_db": eb_o,
+                             "precision": prec_o, "ms_per_decode": ms_o,
+                             "coded_Gbit_s": B_o * H_o.n / (ms_o / 1e3) / 1e9,
+                             "mean_iterations": its_o.mean().item(), "max_iterations_used": its_o.max().item(),
+                             "n": H_o.n, "edges": H_o.total_edges}
             del P_o, ws_o, outs_o
+        if "C4" in others and "C4_fast_fp32" in others:
+            others["C4_fast_fp32"]["speedup_vs_exact"] = others["C4"]["ms_per_decode"] / others["C4_fast_fp32"]["ms_per_decode"]
+        if "C2" in others and "C2_fixed" in others:
+            others["C2"]["vs_fixed_iterations"] = others["C2"]["ms_per_decode"] / others["C2_fixed"]["ms_per_decode"]
         # the reference-facing single-frame call at C3 (engine.py:363 decode(y, sigma2)): host in,
         # host out, wall clock; one cooperative grid launch per frame (grid.cu)
         Y1, s2_1 = synthetic_observations(H, 12, args.ebno, seed=77)

@@ -77,6 +77,7 @@ size_t workspace_bytes(const ldpc_graph *g, int32_t B) {
     b += align256(sizeof(uint32_t) * NW) * 2;
     b += align256(sizeof(int32_t) * Bp);
     b += align256(sizeof(float) * (size_t)kOdScratchBlocks * fast_od_scratch_stride(g));
+    b += align256(sizeof(int32_t) * Bp) * 3 + align256(sizeof(uint32_t) * NW) + align256(sizeof(int32_t) * 8);
     return b;
 }
 
@@ -108,6 +109,11 @@ int carve_workspace(const ldpc_graph *g, int32_t B, void *ws, size_t bytes, Work
     w->iters = (int32_t *)take(sizeof(int32_t) * w->Bp);
     w->od_stride = fast_od_scratch_stride(g);
     w->od_scratch = w->od_stride ? (float *)take(sizeof(float) * (size_t)kOdScratchBlocks * w->od_stride) : nullptr;
+    w->orig = (int32_t *)take(sizeof(int32_t) * w->Bp);
+    w->ret_orig = (int32_t *)take(sizeof(int32_t) * w->Bp);
+    w->perm = (int32_t *)take(sizeof(int32_t) * w->Bp);
+    w->ret_sel = (uint32_t *)take(sizeof(uint32_t) * w->NW);
+    w->ctl = (int32_t *)take(sizeof(int32_t) * 8);
     return LDPC_OK;
 }
 
@@ -195,12 +201,12 @@ struct Prof {
 
 NodeLaunch check_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
     return NodeLaunch{g->chk_off, g->chk_var, g->chk_order, 0, 0, w.msg, w.P, nullptr, done, w.Bp, w.NWs,
-                      (int32_t)g->E, g->n, g->chk_slot, g->chk_slot_ord, g->chk_var_ord, 0, w.scratch};
+                      (int32_t)g->E, g->n, g->chk_slot, g->chk_slot_ord, g->chk_var_ord, 0, w.scratch, 0, w.act};
 }
 
 NodeLaunch var_args(const ldpc_graph *g, const Workspace &w, const uint32_t *done) {
     return NodeLaunch{g->var_off, nullptr, g->var_order, 0, 0, w.msg, w.P, w.chat, done, w.Bp, w.NWs,
-                      (int32_t)g->E, g->n, g->var_slot, g->var_slot_ord, nullptr, 0, w.scratch};
+                      (int32_t)g->E, g->n, g->var_slot, g->var_slot_ord, nullptr, 0, w.scratch, 0, w.act};
 }
 
 // fp32 fast mode (LDPC_FLAG_FP32): fp32 messages and priors live in the fp64 message buffer
@@ -336,10 +342,21 @@ int init_flags(const Workspace &w, bool early, cudaStream_t s, int32_t chat_rows
 
 }  // namespace
 
+// Early-stop compaction (compact.cu): compact when the live codewords fit in at most this percent
+// of the active chunks; LDPC_COMPACT=0 disables it, LDPC_COMPACT=<pct> sets the threshold.
+static int compact_pct() {
+    static const int v = [] {
+        const char *e = getenv("LDPC_COMPACT");
+        return e ? std::max(0, std::min(100, atoi(e))) : 75;
+    }();
+    return v;
+}
+
 // Algorithm 2 (serial.py:165-178) on one view of the workspace: the whole batch
-// (streaming schedule) or one tile (tiled schedule).
+// (streaming schedule) or one tile (tiled schedule).  `out` != nullptr: early stop with
+// compaction, retired codewords' results written to the caller's outputs as they stop.
 static int decode_view(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s,
-                       Prof &prof, bool fast) {
+                       Prof &prof, bool fast, const DecodeOut *out = nullptr) {
     g_sweep = 0;  // every decode (and so every captured graph) uses the same direction sequence
     const int64_t B = w.B, E = g->E, n = g->n, m = g->m;
     const int64_t wb = fast ? 4 : 8;                         // message / prior width in bytes
@@ -354,6 +371,14 @@ static int decode_view(const ldpc_graph *g, const Workspace &w, int32_t max_iter
         if (early) {
             RUN(LDPC_KCLASS_SYNDROME, s_bytes, launch_syndrome(g, w, false, true, s));
             RUN(LDPC_KCLASS_SYNDROME, 0, launch_update_done(w, t - 1, false, s));
+        }
+        if (out != nullptr) {
+            // the state that crosses into round t: q (messages) and the priors
+            // (the fp32 fast mode moves its fp32 messages and priors, and the fp64 priors its O(d)
+            // variable kernels read)
+            const CompactArray exact[2] = {{w.msg, (int32_t)E, 8}, {w.P, (int32_t)n, 8}};
+            const CompactArray f32[3] = {{msg32(g, w), (int32_t)E, 4}, {prior32(g, w), (int32_t)n, 4}, {w.P, (int32_t)n, 8}};
+            RUN(LDPC_KCLASS_LAYOUT, 0, launch_compact(g, w, compact_pct(), *out, fast ? f32 : exact, fast ? 3 : 2, s));
         }
         RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, false, done, s, fast));
     }
@@ -387,9 +412,9 @@ static int32_t tile_groups(const ldpc_graph *g, const Workspace &w, bool fast) {
     return std::min(T, groups);
 }
 
-// The decode proper on a carved workspace whose P is filled.
+// The decode proper on a carved workspace whose P is filled, then the caller's outputs.
 int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool early, cudaStream_t s, Prof &prof,
-               bool fast = false) {
+               bool fast, const DecodeOut &out) {
     int rc = init_flags(w, early, s, g->n, g->max_dv > kMaxMidVarDegree);
     if (rc) return rc;
     if (fast) {
@@ -397,12 +422,26 @@ int run_decode(const ldpc_graph *g, const Workspace &w, int32_t max_iter, bool e
         if (rc) return rc;
     }
     const int32_t T = tile_groups(g, w, fast);
-    if (T == 0) return decode_view(g, w, max_iter, early, s, prof, fast);
-    const int32_t groups = (w.B + 31) / 32;
-    for (int32_t g0 = 0; g0 < groups; g0 += T) {
-        rc = decode_view(g, tile_view(g, w, g0, std::min(T, groups - g0)), max_iter, early, s, prof, fast);
-        if (rc) return rc;
+    const int64_t n = g->n, m = g->m, B = w.B;
+    if (T == 0 && early && compact_pct() > 0 && w.Bp > kBatchAlign) {
+        RUN(LDPC_KCLASS_LAYOUT, 0, launch_compact_init(w, s));
+        Workspace wc = w;
+        wc.act = w.ctl;  // node kernels cover the active chunks only
+        if ((rc = decode_view(g, wc, max_iter, early, s, prof, fast, &out))) return rc;
+        RUN(LDPC_KCLASS_LAYOUT, (n / 8) * 2 * B + (out.syn ? (m / 8) * 2 * B : 0), launch_compact_finish(g, w, out, s));
+        return LDPC_OK;
     }
+    if (T == 0) {
+        rc = decode_view(g, w, max_iter, early, s, prof, fast);
+    } else {
+        const int32_t groups = (w.B + 31) / 32;
+        for (int32_t g0 = 0; g0 < groups && rc == LDPC_OK; g0 += T)
+            rc = decode_view(g, tile_view(g, w, g0, std::min(T, groups - g0)), max_iter, early, s, prof, fast);
+    }
+    if (rc) return rc;
+    RUN(LDPC_KCLASS_LAYOUT, (n / 8) * 2 * B, launch_pack_rows(w.chat, g->n, w.NW, w.B, out.est, s));
+    if (out.syn) RUN(LDPC_KCLASS_LAYOUT, (m / 8) * 2 * B, launch_pack_rows(w.zb, g->m, w.NW, w.B, out.syn, s));
+    RUN(LDPC_KCLASS_LAYOUT, 0, launch_finalize(w, early, max_iter, out.success, out.iters, s));
     return LDPC_OK;
 }
 
@@ -472,13 +511,8 @@ static int decode_impl(const ldpc_graph *g, const double *p_dev, const double *s
     auto sequence = [&](Prof &prof) -> int {
         const int64_t n = g->n, m = g->m;
         RUN(LDPC_KCLASS_LAYOUT, 16 * n * B, launch_transpose_priors(p_dev, sig2, B, g->n, w.P, w.Bp, s));
-        int r = run_decode(g, w, max_iterations, early, s, prof, fast);
-        if (r) return r;
-        RUN(LDPC_KCLASS_LAYOUT, (n / 8) * 2 * B, launch_pack_rows(w.chat, g->n, w.NW, B, est_bits_dev, s));
-        if (syn_bits_dev)
-            RUN(LDPC_KCLASS_LAYOUT, (m / 8) * 2 * B, launch_pack_rows(w.zb, g->m, w.NW, B, syn_bits_dev, s));
-        RUN(LDPC_KCLASS_LAYOUT, 0, launch_finalize(w, early, max_iterations, success_dev, iters_dev, s));
-        return LDPC_OK;
+        return run_decode(g, w, max_iterations, early, s, prof, fast,
+                          DecodeOut{est_bits_dev, success_dev, iters_dev, syn_bits_dev});
     };
     Prof prof;
     prof.out = prof_host;
@@ -604,10 +638,8 @@ extern "C" int ldpc_decode_channel(const ldpc_graph *g, uint64_t seed, uint64_t 
     if (rc) return rc;
     Prof prof;
     if ((rc = launch_channel_priors(seed, point, frame0, B, g->n, sigma2, w.P, w.Bp, s))) return rc;
-    if ((rc = run_decode(g, w, max_iterations, early, s, prof, fast))) return rc;
-    if ((rc = launch_pack_rows(w.chat, g->n, w.NW, B, est_bits_dev, s))) return rc;
-    if (syn_bits_dev && (rc = launch_pack_rows(w.zb, g->m, w.NW, B, syn_bits_dev, s))) return rc;
-    return launch_finalize(w, early, max_iterations, success_dev, iters_dev, s);
+    return run_decode(g, w, max_iterations, early, s, prof, fast,
+                      DecodeOut{est_bits_dev, success_dev, iters_dev, syn_bits_dev});
 }
 
 extern "C" int ldpc_count_errors(const ldpc_graph *g, const uint32_t *est_bits_dev, const uint8_t *success_dev,

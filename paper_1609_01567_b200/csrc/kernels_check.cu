@@ -71,7 +71,9 @@ __global__ void __launch_bounds__(kThreads) k_check_reg(NodeLaunch a) {
     const int lane = threadIdx.x & 31;
     // grid (node blocks, codeword chunks): blocks are dispatched x-fastest, so
     // the grid sweeps all nodes of chunk 0, then chunk 1, ... (chunk-major)
-    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int nch = active_chunks(a, (int)gridDim.y, 32 * V);
+    if ((int)blockIdx.y >= nch) return;
+    const int ch = a.reverse ? nch - 1 - (int)blockIdx.y : (int)blockIdx.y;
     const int ni = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (ni >= a.node_count) return;
     if (chunk_done<V>(a.done, ch)) return;

@@ -27,7 +27,9 @@ template <int D, bool FROM_PRIOR>
 __global__ void __launch_bounds__(kThreads) k_check_f32(NodeLaunch a, float *msg, const float *P) {
     const int lane = threadIdx.x & 31;
     // grid (node blocks, codeword chunks), dispatched x-fastest: chunk-major sweep
-    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int nch = active_chunks(a, (int)gridDim.y, 64);
+    if ((int)blockIdx.y >= nch) return;
+    const int ch = a.reverse ? nch - 1 - (int)blockIdx.y : (int)blockIdx.y;
     const int ni = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (ni >= a.node_count) return;
     if (a.done != nullptr) {
@@ -70,7 +72,9 @@ template <int D, bool WRITE_Q>
 __global__ void __launch_bounds__(kThreads) k_var_f32(NodeLaunch a, float *msg, const float *P) {
     const int lane = threadIdx.x & 31;
     // grid (node blocks, codeword chunks), dispatched x-fastest: chunk-major sweep
-    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int nch = active_chunks(a, (int)gridDim.y, 64);
+    if ((int)blockIdx.y >= nch) return;
+    const int ch = a.reverse ? nch - 1 - (int)blockIdx.y : (int)blockIdx.y;
     const int ni = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (ni >= a.node_count) return;
     if (a.done != nullptr) {

@@ -325,6 +325,9 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
     const int lane = threadIdx.x & 31;
     int *ids = reinterpret_cast<int *>(wsm);                          // [S][kIdsStride]
     double *rows = reinterpret_cast<double *>(wsm + R::kIdsBytes);    // [S][ROWS][ROW]
+    // early-stop compaction: only the active chunks' tasks (chunk-major, so a prefix of the tasks)
+    const int wchunks = active_chunks(a, a.Bp / (32 * V), 32 * V);
+    ntasks = min(ntasks, (int64_t)a.node_count * wchunks);
     if (first >= ntasks) return;
     const int ntask = (int)((ntasks - first + W - 1) / W);  // this warp's tasks: first, first + W, ...
 
@@ -332,7 +335,7 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
     // issued), so the index loads' L2 latency is off the critical path; the
     // cursor runs two tasks ahead of the issue.
     TaskCursor cur(first, W, a.node_count);
-    const int chunks_m1 = a.Bp / (32 * V) - 1;  // reverse sweep: chunk c -> chunks-1-c
+    const int chunks_m1 = wchunks - 1;  // reverse sweep: chunk c -> chunks-1-c
     auto chunk_of = [&](int c) { return a.reverse ? chunks_m1 - c : c; };
     int nid0 = load_id<D, IS_VAR, FP>(a, cur.ni, lane), nch0 = chunk_of(cur.ch);
     DoneMask nd0 = EARLY ? load_done<V>(a.done, nch0) : DoneMask{};

@@ -66,7 +66,9 @@ template <int D, int V, bool WRITE_Q>
 __global__ void __launch_bounds__(kThreads, (D <= 2 && V == 2) ? 5 : 1) k_var_reg(NodeLaunch a) {
     const int lane = threadIdx.x & 31;
     // grid (node blocks, codeword chunks), dispatched x-fastest: chunk-major sweep
-    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int nch = active_chunks(a, (int)gridDim.y, 32 * V);
+    if ((int)blockIdx.y >= nch) return;
+    const int ch = a.reverse ? nch - 1 - (int)blockIdx.y : (int)blockIdx.y;
     const int ni = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (ni >= a.node_count) return;
     if (a.done != nullptr) {

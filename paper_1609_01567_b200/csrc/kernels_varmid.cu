@@ -31,7 +31,9 @@ __global__ void __launch_bounds__(32 * mid_warps<MAXD>()) k_var_mid(NodeLaunch a
     constexpr int kMidWarps = mid_warps<MAXD>();
     extern __shared__ __align__(16) double mid_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int nch = active_chunks(a, (int)gridDim.y, 32);
+    if ((int)blockIdx.y >= nch) return;
+    const int ch = a.reverse ? nch - 1 - (int)blockIdx.y : (int)blockIdx.y;
     const int ni = blockIdx.x * kMidWarps + warp;
     if (ni >= a.node_count) return;
     uint32_t dmask = 0;
@@ -133,7 +135,9 @@ __global__ void __launch_bounds__(128) k_check_mid(NodeLaunch a, int D) {
     constexpr int MAXD = 64, kW = 4;
     extern __shared__ __align__(16) double mid_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ch = a.reverse ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
+    const int nch = active_chunks(a, (int)gridDim.y, 32);
+    if ((int)blockIdx.y >= nch) return;
+    const int ch = a.reverse ? nch - 1 - (int)blockIdx.y : (int)blockIdx.y;
     const int ni = blockIdx.x * kW + warp;
     if (ni >= a.node_count) return;
     if (EARLY && a.done[ch] == 0xffffffffu) return;

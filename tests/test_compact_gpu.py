@@ -1,0 +1,90 @@
+"""Per-codeword early stop (serial.py:169-177, engine.py:341-347): live codewords are compacted
+into dense chunks on the device (compact.cu) so the work follows each codeword's stopping round.
+Results must be bit-identical to the oracle and to the uncompacted decode, whatever the
+compaction points are (LDPC_COMPACT=<pct> threshold, 0 = off; read once per process)."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_1609_01567_b200 import CodeTables, ParallelDecoder, configs, priors_awgn_batch
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(code, B, ebno, seed):
+    H = configs.code(code)
+    s2 = configs.ebno_to_sigma2(ebno, configs.rate(H))
+    rng = np.random.default_rng(seed)
+    return H, priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((B, H.n)), s2)
+
+
+@pytest.mark.parametrize("code,B,ebno,iters", [
+    ("C2", 512, 2.0, 20),
+    ("C2", 200, 1.5, 20),
+    ("C1", 700, 1.5, 50),
+    ("C4", 130, 3.0, 20),
+])
+def test_compacted_decode_vs_oracle(cuda, code, B, ebno, iters):
+    from oracle import OracleTables
+
+    H, P = _frames(code, B, ebno, seed=B + iters)
+    with ParallelDecoder(CodeTables.from_matrix(H), max_batch=B) as dec:
+        res = dec.decode_priors(P, iters, schedule="stream")
+    est, ok, its, z = OracleTables.from_matrix(H).decode_batch(P, iters)
+    assert len(set(its.tolist())) > 3  # codewords stop at many different rounds
+    assert np.array_equal(res.iterations, its)
+    assert np.array_equal(res.success.astype(bool), ok)
+    assert np.array_equal(res.estimates(), est)
+    assert np.array_equal(res.syndromes(), z)
+
+
+_RUN = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_1609_01567_b200 import CodeTables, ParallelDecoder, configs, priors_awgn_batch
+H = configs.code({code!r})
+s2 = configs.ebno_to_sigma2({ebno}, configs.rate(H))
+P = priors_awgn_batch(-1.0 + np.sqrt(s2) * np.random.default_rng(4).standard_normal(({B}, H.n)), s2)
+out = {{}}
+with ParallelDecoder(CodeTables.from_matrix(H), max_batch={B}) as dec:
+    for prec in ("fp64", "fp32"):
+        r = dec.decode_priors(P, {iters}, precision=prec, schedule="stream")
+        out[prec + "_est"], out[prec + "_syn"] = r.est_bits, r.syn_bits
+        out[prec + "_ok"], out[prec + "_it"] = r.success, r.iterations
+        e, o, i, z = dec.decode_device(torch.from_numpy(P).cuda(), {iters}, precision=prec)
+        torch.cuda.synchronize()
+        out[prec + "_dev_est"], out[prec + "_dev_it"] = e.cpu().numpy(), i.cpu().numpy()
+    # device channel (f1) through the same decode sequence
+    d = dec.alloc_outputs({B}, torch.device("cuda"))
+    dec.decode_channel(7, 0, 0, {B}, s2, {iters}, outputs=d)
+    torch.cuda.synchronize()
+    out["chan_est"], out["chan_it"] = d[0].cpu().numpy(), d[2].cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def _run(tmp_path, env_value, code, B, ebno, iters):
+    path = str(tmp_path / f"out_{env_value}.npz")
+    env = dict(os.environ, LDPC_COMPACT=env_value)
+    src = _RUN.format(root=str(ROOT), code=code, B=B, ebno=ebno, iters=iters, path=path)
+    r = subprocess.run([sys.executable, "-c", src], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(path)
+
+
+@pytest.mark.parametrize("code,B,ebno,iters", [("C2", 448, 2.0, 20), ("C4", 192, 3.0, 20)])
+def test_compaction_points_do_not_change_results(cuda, tmp_path, code, B, ebno, iters):
+    # off, the default threshold, and compaction at every round that frees a chunk
+    runs = {v: _run(tmp_path, v, code, B, ebno, iters) for v in ("0", "75", "100")}
+    base = runs["0"]
+    assert len(set(base["fp64_it"].tolist())) > 3
+    for v in ("75", "100"):
+        for k in base.files:
+            assert np.array_equal(runs[v][k], base[k]), (v, k)
