@@ -29,12 +29,22 @@ constexpr int kPlanThreads = 1024;
 
 // ctl[0] = active 64-codeword chunks, ctl[1] = compact this round, ctl[2] = L (live codewords),
 // ctl[3] = first output chunk whose contents change, ctl[4] = active chunks before this round's plan
-__global__ void __launch_bounds__(kPlanThreads) k_compact_plan(uint32_t *done, int32_t *orig, int32_t *ret_orig,
-                                                               int32_t *perm, uint32_t *ret_sel, int32_t *ctl,
-                                                               int frac_pct) {
+// The plan also does the early-stop update of round `round` first (k_update_done's work,
+// serial.py:169-177: codewords whose syndrome is all-zero stop now with iterations_used = round).
+__global__ void __launch_bounds__(kPlanThreads) k_compact_plan(uint32_t *done, uint32_t *unsat, int32_t *iters,
+                                                               int32_t NW, int32_t round, int32_t *orig,
+                                                               int32_t *ret_orig, int32_t *perm, uint32_t *ret_sel,
+                                                               int32_t *ctl, int frac_pct) {
     __shared__ int scan[kPlanThreads];
     __shared__ int first_moved;
     const int t = threadIdx.x;
+    for (int w = t; w < NW; w += kPlanThreads) {
+        const uint32_t d = done[w], newly = ~d & ~unsat[w];
+        for (uint32_t x = newly; x; x &= x - 1) iters[32 * w + __ffs(x) - 1] = round;
+        done[w] = d | newly;
+        unsat[w] = 0;
+    }
+    __syncthreads();
     const int act = ctl[0];
     const int NWa = 2 * act;  // active done words
     const int per = (NWa + kPlanThreads - 1) / kPlanThreads;
@@ -238,12 +248,13 @@ int launch_compact_init(const Workspace &w, cudaStream_t s) {
     return LDPC_OK;
 }
 
-// One compaction point (after the early-stop update of a round): the plan, then one launch that
+// One compaction point (after the syndrome of a round): the early-stop update and the plan, then one launch that
 // retires the stopped codewords and moves the rows of the state arrays (msg, priors, ...).
-int launch_compact(const ldpc_graph *g, const Workspace &w, int frac_pct, const DecodeOut &out,
+int launch_compact(const ldpc_graph *g, const Workspace &w, int32_t round, int frac_pct, const DecodeOut &out,
                    const CompactArray *arrays, int count, cudaStream_t s) {
     LDPC_ARG_CHECK(count >= 1 && count <= 3, "compaction moves 1..3 arrays");
-    k_compact_plan<<<1, kPlanThreads, 0, s>>>(w.done, w.orig, w.ret_orig, w.perm, w.ret_sel, w.ctl, frac_pct);
+    k_compact_plan<<<1, kPlanThreads, 0, s>>>(w.done, w.unsat, w.iters, w.NW, round, w.orig, w.ret_orig, w.perm,
+                                              w.ret_sel, w.ctl, frac_pct);
     LDPC_CHECK_LAUNCH();
     MoveArrays arr{};
     int64_t rows = 0;

@@ -370,15 +370,15 @@ static int decode_view(const ldpc_graph *g, const Workspace &w, int32_t max_iter
         RUN(LDPC_KCLASS_VARIABLE, ve_bytes, var_phase(g, w, true, done, s, fast));
         if (early) {
             RUN(LDPC_KCLASS_SYNDROME, s_bytes, launch_syndrome(g, w, false, true, s));
-            RUN(LDPC_KCLASS_SYNDROME, 0, launch_update_done(w, t - 1, false, s));
+            if (out == nullptr) RUN(LDPC_KCLASS_SYNDROME, 0, launch_update_done(w, t - 1, false, s));
         }
-        if (out != nullptr) {
+        if (out != nullptr) {  // (the compaction plan does the early-stop update of round t - 1 first)
             // the state that crosses into round t: q (messages) and the priors
             // (the fp32 fast mode moves its fp32 messages and priors, and the fp64 priors its O(d)
             // variable kernels read)
             const CompactArray exact[2] = {{w.msg, (int32_t)E, 8}, {w.P, (int32_t)n, 8}};
             const CompactArray f32[3] = {{msg32(g, w), (int32_t)E, 4}, {prior32(g, w), (int32_t)n, 4}, {w.P, (int32_t)n, 8}};
-            RUN(LDPC_KCLASS_LAYOUT, 0, launch_compact(g, w, compact_pct(), *out, fast ? f32 : exact, fast ? 3 : 2, s));
+            RUN(LDPC_KCLASS_LAYOUT, 0, launch_compact(g, w, t - 1, compact_pct(), *out, fast ? f32 : exact, fast ? 3 : 2, s));
         }
         RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, false, done, s, fast));
     }
