@@ -411,7 +411,7 @@ def run_ours(args):
                   if k in ("check", "variable", "estimate") and v["ms"] > 0}
 
     # e2e through the public host API: pinned priors in, packed results out, every step
-    e2e = e2e_stream = e2e_from_y = None
+    e2e = e2e_stream = e2e_from_y = e2e_pageable = None
     if not args.no_e2e:
         from paper_1609_01567_b200.decoder import BatchResult
 
@@ -439,6 +439,28 @@ def run_ours(args):
                "ms_per_step": 1e3 * el / args.steps,
                "path": "ParallelDecoder.decode_priors (ldpc_decoder_decode_host: pinned H2D, decode, D2H; "
                        "geometric sub-batches over a copy stream and two compute streams)"}
+        # the same call as a plain caller makes it (engine.py:363-372 takes any array): pageable numpy
+        # priors in, fresh (pageable) result arrays out; staged through the decoder's pinned slots
+        Pn_pageable = np.array(Pn, copy=True)
+        for _ in range(max(1, args.warmup)):
+            dec.decode_priors(Pn_pageable, iters, early_stop=False)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            dec.decode_priors(Pn_pageable, iters, early_stop=False)
+        el_pg = time.perf_counter() - t0
+        tp = torch.tensor([el_pg], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+        el_pg = float(tp.item())
+        e2e_pageable = {"value": world * B * n * args.steps / el_pg / 1e9, "unit": UNIT,
+                        "h2d_bytes_per_step": int(Pn_pageable.nbytes), "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                        "ms_per_step": 1e3 * el_pg / args.steps,
+                        "vs_pinned": e2e["ms_per_step"] / (1e3 * el_pg / args.steps),
+                        "path": "ParallelDecoder.decode_priors on a plain numpy array, fresh numpy results "
+                                "(pageable input staged through pinned slots by host copy threads, overlapped "
+                                "with the H2D DMA; results through pinned buffers)"}
         # streaming API (two batches in flight: the H2D of step k+1 overlaps the decode of step k)
         outs2 = [res, BatchResult(pin((B, (n + 31) // 32), torch.int32).view(np.uint32), pin((B,), torch.uint8),
                                   pin((B,), torch.int32), pin((B, (m + 31) // 32), torch.int32).view(np.uint32),
@@ -607,6 +629,7 @@ def run_ours(args):
             "e2e": e2e,
             "e2e_stream": e2e_stream,
             "e2e_from_y": e2e_from_y,
+            "e2e_pageable": e2e_pageable,
             "fast_fp32": fast,
             "other_configs": others,
             "gpu_launches": int(launches),

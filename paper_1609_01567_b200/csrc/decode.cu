@@ -14,8 +14,10 @@
 // stopped skip their work.  All control stays on the device: no host sync
 // between rounds.
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include "common.cuh"
 
@@ -752,7 +754,85 @@ int e2e_lanes() {
 }
 }
 
+// Host threads that copy between pageable (user) and pinned (staging) memory in parallel slices;
+// the calling thread copies the first slice itself.
+struct CopyPool {
+    std::vector<std::thread> th;
+    std::mutex mu;
+    std::condition_variable go, fin;
+    char *dst = nullptr;
+    const char *src = nullptr;
+    size_t bytes = 0;
+    uint64_t gen = 0;
+    int pending = 0;
+    bool stop = false;
+
+    int parts() const { return (int)th.size() + 1; }
+    void slice(int i, char *d, const char *s, size_t n) const {
+        const size_t per = (n / parts() + 4095) & ~(size_t)4095;
+        const size_t lo = std::min(n, per * i), hi = std::min(n, lo + per);
+        if (hi > lo) memcpy(d + lo, s + lo, hi - lo);
+    }
+    void start(int workers) {
+        for (int i = 1; i <= workers; i++)
+            th.emplace_back([this, i] {
+                uint64_t seen = 0;
+                for (;;) {
+                    std::unique_lock<std::mutex> lk(mu);
+                    go.wait(lk, [&] { return stop || gen != seen; });
+                    if (stop) return;
+                    seen = gen;
+                    char *d = dst;
+                    const char *s = src;
+                    const size_t n = bytes;
+                    lk.unlock();
+                    slice(i, d, s, n);
+                    lk.lock();
+                    if (--pending == 0) fin.notify_one();
+                }
+            });
+    }
+    void copy(void *d, const void *s, size_t n) {
+        if (th.empty() || n < (1u << 20)) {
+            memcpy(d, s, n);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            dst = static_cast<char *>(d);
+            src = static_cast<const char *>(s);
+            bytes = n;
+            pending = (int)th.size();
+            gen++;
+        }
+        go.notify_all();
+        slice(0, static_cast<char *>(d), static_cast<const char *>(s), n);
+        std::unique_lock<std::mutex> lk(mu);
+        fin.wait(lk, [&] { return pending == 0; });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        go.notify_all();
+        for (auto &t : th) t.join();
+    }
+};
+
 struct ldpc_decoder {
+    // pageable host buffers (plain numpy arrays): inputs staged through pinned slots by the copy
+    // pool, overlapped with the H2D DMA of the previous slot; results land in pinned buffers and
+    // are copied out at the end (allocated on first pageable use)
+    static constexpr int kStages = 3;
+    static constexpr size_t kStageBytes = 16u << 20;
+    void *stage[kStages] = {};
+    cudaEvent_t stage_free[kStages] = {};
+    int stage_next = 0;
+    uint32_t *est_pin = nullptr, *syn_pin = nullptr;
+    uint8_t *succ_pin = nullptr;
+    int32_t *its_pin = nullptr;
+    CopyPool pool;
     const ldpc_graph *g = nullptr;
     int32_t max_batch = 0, sub = 0;
     cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -809,6 +889,12 @@ static void decoder_free(ldpc_decoder *d) {
     for (int i = 0; i < kMaxChunks; i++)
         for (cudaEvent_t e : {d->in_ready[i], d->decoded[i]})
             if (e) cudaEventDestroy(e);
+    for (int k = 0; k < ldpc_decoder::kStages; k++) {
+        if (d->stage[k]) cudaFreeHost(d->stage[k]);
+        if (d->stage_free[k]) cudaEventDestroy(d->stage_free[k]);
+    }
+    for (void *h : {(void *)d->est_pin, (void *)d->syn_pin, (void *)d->succ_pin, (void *)d->its_pin})
+        if (h) cudaFreeHost(h);
     for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_comp[2], d->s_comp[3], d->s_out})
         if (s) cudaStreamDestroy(s);
     delete d;
@@ -905,6 +991,48 @@ extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32
     return LDPC_OK;
 }
 
+static bool host_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+static int staging_alloc(ldpc_decoder *d) {
+    if (d->stage[0] != nullptr) return LDPC_OK;
+    const size_t MB = (size_t)d->max_batch, RWn = (d->g->n + 31) / 32, RWm = (d->g->m + 31) / 32;
+    for (int k = 0; k < ldpc_decoder::kStages; k++) {
+        LDPC_CUDA_TRY(cudaHostAlloc(&d->stage[k], ldpc_decoder::kStageBytes, cudaHostAllocDefault));
+        LDPC_CUDA_TRY(cudaEventCreateWithFlags(&d->stage_free[k], cudaEventDisableTiming));
+    }
+    LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->est_pin, sizeof(uint32_t) * RWn * MB, cudaHostAllocDefault));
+    LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->syn_pin, sizeof(uint32_t) * RWm * MB, cudaHostAllocDefault));
+    LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->succ_pin, MB, cudaHostAllocDefault));
+    LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->its_pin, sizeof(int32_t) * MB, cudaHostAllocDefault));
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    d->pool.start((int)std::min(7u, std::max(1u, hw / 2) - 1));  // + the calling thread
+    return LDPC_OK;
+}
+
+// pageable host -> device through the pinned slots: copy a slot's piece on the host threads once its
+// previous DMA is done, then its DMA on the copy stream (the next piece's host copy overlaps it)
+static cudaError_t stage_in(ldpc_decoder *d, void *dst_dev, const void *src_host, size_t bytes) {
+    for (size_t off = 0; off < bytes; off += ldpc_decoder::kStageBytes) {
+        const size_t len = std::min(ldpc_decoder::kStageBytes, bytes - off);
+        const int k = d->stage_next;
+        d->stage_next = (k + 1) % ldpc_decoder::kStages;
+        cudaError_t e = cudaEventSynchronize(d->stage_free[k]);
+        if (e != cudaSuccess) return e;
+        d->pool.copy(d->stage[k], static_cast<const char *>(src_host) + off, len);
+        e = cudaMemcpyAsync(static_cast<char *>(dst_dev) + off, d->stage[k], len, cudaMemcpyHostToDevice, d->s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(d->stage_free[k], d->s_in);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 static int decoder_run(ldpc_decoder *d, const double *p_host, const double *s2_host, int32_t B,
                        int32_t max_iterations, uint32_t flags, uint32_t *est_bits_host, uint8_t *success_host,
                        int32_t *iters_host, uint32_t *syn_bits_host) {
@@ -932,18 +1060,38 @@ static int decoder_run(ldpc_decoder *d, const double *p_host, const double *s2_h
             set_error("%s: %s", what, cudaGetErrorString(x));
         }
     };
-    // 1. every H2D copy, back to back on the copy stream
+    // Plain (pageable) host arrays, as the reference API's callers pass them (engine.py:363-372), go
+    // through pinned staging: a pageable cudaMemcpyAsync would be staged by the driver one
+    // synchronous piece at a time.
+    const bool in_pinned = host_pinned(p_host);  // (sigma2, B doubles, is copied as it is)
+    const bool out_pinned = host_pinned(est_bits_host) && host_pinned(success_host) && host_pinned(iters_host) &&
+                            (syn_bits_host == nullptr || host_pinned(syn_bits_host));
+    if (!in_pinned || !out_pinned) {
+        rc = staging_alloc(d);
+        if (rc) return rc;
+    }
+    uint32_t *est_dst = out_pinned ? est_bits_host : d->est_pin;
+    uint8_t *succ_dst = out_pinned ? success_host : d->succ_pin;
+    int32_t *its_dst = out_pinned ? iters_host : d->its_pin;
+    uint32_t *syn_dst = (out_pinned || syn_bits_host == nullptr) ? syn_bits_host : d->syn_pin;
+    // 1. pinned input: every H2D copy, back to back on the copy stream
     if (s2_host)
         cuda(cudaMemcpyAsync(d->s2, s2_host, sizeof(double) * B, cudaMemcpyHostToDevice, d->s_in), "H2D sigma2");
-    for (size_t i = 0, c0 = 0; i < plan.size(); c0 += plan[i], i++) {
-        cuda(cudaMemcpyAsync(d->p + c0 * n, p_host + c0 * n, sizeof(double) * n * plan[i], cudaMemcpyHostToDevice,
-                             d->s_in), s2_host ? "H2D observations" : "H2D priors");
-        cuda(cudaEventRecord(d->in_ready[i], d->s_in), "record");
-    }
-    // 2. decodes in order, each results copy right behind its decode
+    if (in_pinned)
+        for (size_t i = 0, c0 = 0; i < plan.size(); c0 += plan[i], i++) {
+            cuda(cudaMemcpyAsync(d->p + c0 * n, p_host + c0 * n, sizeof(double) * n * plan[i], cudaMemcpyHostToDevice,
+                                 d->s_in), s2_host ? "H2D observations" : "H2D priors");
+            cuda(cudaEventRecord(d->in_ready[i], d->s_in), "record");
+        }
+    // 2. decodes in order, each results copy right behind its decode (pageable input: each
+    //    sub-batch staged just before its decode is enqueued)
     for (size_t i = 0, c0 = 0; i < plan.size() && rc == LDPC_OK && e == cudaSuccess; c0 += plan[i], i++) {
         const int32_t b = plan[i];
         const int l = (int)(i % d->lanes);
+        if (!in_pinned) {
+            cuda(stage_in(d, d->p + c0 * n, p_host + c0 * n, sizeof(double) * n * b), "H2D (staged)");
+            cuda(cudaEventRecord(d->in_ready[i], d->s_in), "record");
+        }
         cuda(cudaStreamWaitEvent(d->s_comp[l], d->in_ready[i], 0), "wait input");
         if (e != cudaSuccess) break;
         rc = decode_impl(g, d->p + c0 * n, s2_host ? d->s2 + c0 : nullptr, b, max_iterations, flags,
@@ -952,17 +1100,23 @@ static int decoder_run(ldpc_decoder *d, const double *p_host, const double *s2_h
         if (rc) break;
         cuda(cudaEventRecord(d->decoded[i], d->s_comp[l]), "record");
         cuda(cudaStreamWaitEvent(d->s_out, d->decoded[i], 0), "wait decode");
-        cuda(cudaMemcpyAsync(est_bits_host + c0 * RWn, d->est + c0 * RWn, sizeof(uint32_t) * RWn * b,
+        cuda(cudaMemcpyAsync(est_dst + c0 * RWn, d->est + c0 * RWn, sizeof(uint32_t) * RWn * b,
                              cudaMemcpyDeviceToHost, d->s_out), "D2H estimate");
-        cuda(cudaMemcpyAsync(success_host + c0, d->succ + c0, b, cudaMemcpyDeviceToHost, d->s_out), "D2H success");
-        cuda(cudaMemcpyAsync(iters_host + c0, d->its + c0, sizeof(int32_t) * b, cudaMemcpyDeviceToHost, d->s_out),
+        cuda(cudaMemcpyAsync(succ_dst + c0, d->succ + c0, b, cudaMemcpyDeviceToHost, d->s_out), "D2H success");
+        cuda(cudaMemcpyAsync(its_dst + c0, d->its + c0, sizeof(int32_t) * b, cudaMemcpyDeviceToHost, d->s_out),
              "D2H iterations");
         if (syn_bits_host)
-            cuda(cudaMemcpyAsync(syn_bits_host + c0 * RWm, d->syn + c0 * RWm, sizeof(uint32_t) * RWm * b,
+            cuda(cudaMemcpyAsync(syn_dst + c0 * RWm, d->syn + c0 * RWm, sizeof(uint32_t) * RWm * b,
                                  cudaMemcpyDeviceToHost, d->s_out), "D2H syndrome");
     }
     for (cudaStream_t s : {d->s_in, d->s_comp[0], d->s_comp[1], d->s_comp[2], d->s_comp[3], d->s_out})
         if (s) cuda(cudaStreamSynchronize(s), "decode");
+    if (!out_pinned && rc == LDPC_OK && e == cudaSuccess) {
+        d->pool.copy(est_bits_host, est_dst, sizeof(uint32_t) * RWn * B);
+        memcpy(success_host, succ_dst, (size_t)B);
+        memcpy(iters_host, its_dst, sizeof(int32_t) * B);
+        if (syn_bits_host) d->pool.copy(syn_bits_host, syn_dst, sizeof(uint32_t) * RWm * B);
+    }
     if (rc == LDPC_OK && e != cudaSuccess) rc = LDPC_ECUDA;
     if (rc == LDPC_ECUDA) d->poisoned = true;  // mirrors engine.py:389-392: refuse further use
     return rc;

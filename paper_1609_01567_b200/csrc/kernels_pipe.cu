@@ -22,6 +22,9 @@
 // persistent: warp w of W takes tasks w, w+W, ... in chunk-major order.
 #include <algorithm>
 #include <mutex>
+#include <string>
+
+#include <cuda.h>
 
 #include "common.cuh"
 
@@ -43,12 +46,61 @@ constexpr int ring_stages(int rows) {
 // Per stage: 32 row ids (one per lane), the task's codeword chunk at [32], its skip flag at [33]
 // and its done-mask words at [34..35] (early stop: read with the ids, two issues ahead).
 constexpr int kIdsStride = 36;
-template <int ROWS, int V, int MINB>
+template <int ROWS, int V, int MINB, bool TMA = false>
 struct Ring {
     static constexpr int S = ring_stages<V, MINB>(ROWS);
-    static constexpr size_t kIdsBytes = (size_t)S * kIdsStride * sizeof(int);
+    // TMA: one mbarrier per stage after the ids, and stages 128-byte aligned (bulk-tensor destinations)
+    static constexpr size_t kBarOff = (size_t)S * kIdsStride * sizeof(int);
+    static constexpr size_t kIdsBytes = TMA ? (kBarOff + S * sizeof(uint64_t) + 127) / 128 * 128 : kBarOff;
     static constexpr size_t kBytes = kIdsBytes + (size_t)S * ROWS * 32 * V * sizeof(double);
 };
+
+// ---- TMA (bulk tensor) data movement for the variable ring --------------------
+// The message and prior arrays as 2-D tensors: [Bp/64 * rows][64] fp64 (a 64-codeword chunk row is
+// 512 contiguous bytes); box = one row of a task (32 * V doubles).  One elected lane fetches a task's
+// rows with tile::gather4 (4 rows, given by their indices, per instruction) plus single-row tile
+// loads, completing on the stage's mbarrier (complete_tx), instead of 32 lanes issuing LDGSTS.
+struct __align__(64) TMap {
+    uint64_t v[16];  // CUtensorMap (opaque, 128 bytes)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void tma_gather4(void *dst, const TMap *map, int c0, int r0, int r1, int r2, int r3,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_row(void *dst, const TMap *map, int c0, int r, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r), "r"(smem_u32(bar))
+        : "memory");
+}
 
 
 template <int V>
@@ -164,6 +216,45 @@ __device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *id
         const double *src = (prior_row ? pb : mb) + row_off(src_id);
         if (r < ROWS) cp_async16(dst + r * ROW, src);
     }
+}
+
+// Variables only: the task's D message rows (gather4 in fours, then single rows) and, for low
+// degrees, its prior row, all by lane 0, completing on the stage's mbarrier.
+template <int D, int V, bool EARLY>
+__device__ __forceinline__ void issue_tma(const NodeLaunch &a, double *rows, int *ids_s, uint64_t *bar, int ch,
+                                          int id, const DoneMask &dm, int lane, const TMap *tm_msg,
+                                          const TMap *tm_p) {
+    constexpr int ROWS = ring_rows<D, true>();
+    constexpr int ROW = 32 * V;
+    const bool skip = EARLY && all_done<V>(dm);
+    ids_s[lane] = id;
+    if (lane == 0) {
+        ids_s[32] = ch;
+        if constexpr (EARLY) {
+            ids_s[33] = skip ? 1 : 0;
+            ids_s[34] = (int)dm.w0;
+            ids_s[35] = (int)dm.w1;
+        }
+    }
+    __syncwarp();  // lane 0 reads every lane's row id
+    if (lane != 0) return;
+    if (skip) {  // nothing to fetch: complete the stage's phase without a transaction
+        mbar_arrive(bar);
+        return;
+    }
+    const int c64 = V == 2 ? ch : (ch >> 1);         // 64-codeword chunk of the task
+    const int c0 = V == 2 ? 0 : (ch & 1) * 32;       // its first codeword within the chunk row
+    const int rm = c64 * a.msg_rows, rp = c64 * a.p_rows;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the stage's earlier generic reads
+    mbar_arrive_tx(bar, ROWS * ROW * (uint32_t)sizeof(double));
+    int r = 0;
+#pragma unroll
+    for (; r + 4 <= D; r += 4)
+        tma_gather4(rows + r * ROW, tm_msg, c0, rm + ids_s[r], rm + ids_s[r + 1], rm + ids_s[r + 2], rm + ids_s[r + 3],
+                    bar);
+#pragma unroll
+    for (; r < D; r++) tma_row(rows + r * ROW, tm_msg, c0, rm + ids_s[r], bar);
+    if constexpr (prior_in_ring<D, true>()) tma_row(rows + D * ROW, tm_p, c0, rp + ids_s[D], bar);
 }
 
 template <int D, int V>
@@ -311,20 +402,30 @@ __device__ __forceinline__ void load_prior(const NodeLaunch &a, int node, int ch
 }
 
 // EARLY: early-stop mode (a.done != nullptr): per-task chunk-done masks, read ahead with the ids
-template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY>  // FLAG: FROM_PRIOR / WRITE_Q
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY, bool TMA = false>  // FLAG: FROM_PRIOR / WRITE_Q
 __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, int64_t first, int64_t W,
-                                          unsigned char *wsm) {
+                                          unsigned char *wsm, const TMap *tm_msg = nullptr,
+                                          const TMap *tm_p = nullptr) {
     // one warp's persistent task loop: tasks first, first + W, ... of a side's bucket,
     // its ring (ids + stages) at wsm
+    static_assert(!TMA || IS_VAR, "the TMA ring serves the variable side");
     constexpr int ROWS = ring_rows<D, IS_VAR>();
     constexpr bool PREG = IS_VAR && !prior_in_ring<D, IS_VAR>();  // prior via registers
     constexpr int ROW = 32 * V;
     constexpr bool FP = !IS_VAR && FLAG;
-    using R = Ring<ROWS, V, MINB>;
+    using R = Ring<ROWS, V, MINB, TMA>;
     constexpr int S = R::S;
     const int lane = threadIdx.x & 31;
     int *ids = reinterpret_cast<int *>(wsm);                          // [S][kIdsStride]
     double *rows = reinterpret_cast<double *>(wsm + R::kIdsBytes);    // [S][ROWS][ROW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wsm + R::kBarOff);  // [S] (TMA)
+    if constexpr (TMA) {
+        if (lane == 0) {
+            for (int k = 0; k < S; k++) mbar_init(bars + k, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
     // early-stop compaction: only the active chunks' tasks (chunk-major, so a prefix of the tasks)
     const int wchunks = active_chunks(a, a.Bp / (32 * V), 32 * V);
     ntasks = min(ntasks, (int64_t)a.node_count * wchunks);
@@ -361,7 +462,12 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
             cur.next();
         }
         const int sj = j % S;
-        issue<D, V, IS_VAR, FP, EARLY>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, idone, lane);
+        if constexpr (TMA)
+            issue_tma<D, V, EARLY>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, bars + sj, ich, id, idone,
+                                   lane, tm_msg, tm_p);
+        else
+            issue<D, V, IS_VAR, FP, EARLY>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, idone,
+                                           lane);
     };
     // prologue: copies of tasks 0..S-2 (one commit group per task)
     for (int j = 0; j < S - 1; j++) {
@@ -383,10 +489,15 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
     for (int it = 0; it < ntask; it++) {
         // keep S-1 tasks in flight: issue task it + S-1 into the stage freed last iteration
         if (it + S - 1 < ntask) issue_next(it + S - 1);
-        cp_commit();
-        cp_wait<S - 1>();  // this lane's copies of task it have landed
-        __syncwarp();      // ... and every other lane's (V=1 lanes read pieces copied by other lanes)
         const int s = it % S;
+        if constexpr (TMA) {
+            mbar_wait(bars + s, (uint32_t)(it / S) & 1u);  // the stage's bytes (and lane 0's ids) landed
+            __syncwarp();
+        } else {
+            cp_commit();
+            cp_wait<S - 1>();  // this lane's copies of task it have landed
+            __syncwarp();      // ... and every other lane's (V=1 lanes read pieces copied by other lanes)
+        }
         const int *ids_s = ids + s * kIdsStride;
         const int ch = ids_s[32];
         double pj[V];
@@ -410,7 +521,7 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
         }
         __syncwarp();  // stage s is reused by the issue of the next iteration
     }
-    cp_wait<0>();
+    if constexpr (!TMA) cp_wait<0>();
 }
 
 template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY>  // FLAG: FROM_PRIOR / WRITE_Q
@@ -420,6 +531,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int6
     const int warp = threadIdx.x >> 5;
     ring_loop<D, V, IS_VAR, FLAG, MINB, EARLY>(a, ntasks, (int64_t)blockIdx.x * kWarpsPerBlock + warp,
                                         (int64_t)gridDim.x * kWarpsPerBlock, smem + (size_t)warp * R::kBytes);
+}
+
+template <int D, int V, bool WRITE_Q, int MINB, bool EARLY>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_var_ring_tma(NodeLaunch a, int64_t ntasks, const __grid_constant__ TMap tm_msg, const __grid_constant__ TMap tm_p) {
+    using R = Ring<ring_rows<D, true>(), V, MINB, true>;
+    extern __shared__ __align__(128) unsigned char smem_t[];
+    const int warp = threadIdx.x >> 5;
+    ring_loop<D, V, true, WRITE_Q, MINB, EARLY, true>(a, ntasks, (int64_t)blockIdx.x * kWarpsPerBlock + warp,
+                                                     (int64_t)gridDim.x * kWarpsPerBlock,
+                                                     smem_t + (size_t)warp * R::kBytes, &tm_msg, &tm_p);
 }
 
 // Codewords per lane: V=1 (3 blocks/SM, more warps to hide the fp64 chains) for
@@ -472,11 +594,102 @@ int launch_ring_ve(const NodeLaunch &a, cudaStream_t st) {
     return LDPC_OK;
 }
 
+// ---- host: tensor maps for the TMA ring ----
+using EncodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// [Bp/64 * rows][64] fp64 chunk-major array as a 2-D tensor, box = one task row (32 * V doubles)
+int make_row_map(const double *base, int32_t rows, int32_t Bp, int V, TMap *out) {
+    static EncodeTiled encode = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<EncodeTiled>(fn);
+    }();
+    if (encode == nullptr) {
+        set_error("cuTensorMapEncodeTiled is not available from the driver");
+        return LDPC_ECUDA;
+    }
+    const uint64_t total_rows = (uint64_t)(Bp / 64) * (uint64_t)rows;
+    LDPC_ARG_CHECK(total_rows < (1ull << 31), "TMA ring: %llu rows exceed 32-bit coordinates",
+                   (unsigned long long)total_rows);
+    static_assert(sizeof(TMap) == sizeof(CUtensorMap), "TMap must hold a CUtensorMap");
+    const cuuint64_t dims[2] = {64, total_rows};
+    const cuuint64_t strides[1] = {64 * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)(32 * V), 1};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(reinterpret_cast<CUtensorMap *>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                              const_cast<double *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return LDPC_ECUDA;
+    }
+    return LDPC_OK;
+}
+
+template <int D, int V, bool WRITE_Q, int MINB, bool EARLY>
+int launch_var_tma_ve(const NodeLaunch &a, cudaStream_t st) {
+    constexpr int ROWS = ring_rows<D, true>();
+    const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS, V, MINB, true>::kBytes;
+    auto kern = k_var_ring_tma<D, V, WRITE_Q, MINB, EARLY>;
+    constexpr int kMaxDevices = 64;
+    static int per_sm_of[kMaxDevices] = {}, sms_of[kMaxDevices] = {};
+    static std::mutex mu;
+    int dev = 0;
+    LDPC_CUDA_TRY(cudaGetDevice(&dev));
+    LDPC_ARG_CHECK(dev >= 0 && dev < kMaxDevices, "device ordinal %d out of range", dev);
+    int per_sm, sms;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (per_sm_of[dev] == 0) {
+            LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            LDPC_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
+            int b = 0;
+            LDPC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kThreads, smem));
+            if (b < 1) {
+                set_error("TMA ring kernel (degree %d) does not fit on an SM", D);
+                return LDPC_ECUDA;
+            }
+            per_sm_of[dev] = b;
+        }
+        per_sm = per_sm_of[dev];
+        sms = sms_of[dev];
+    }
+    const int64_t ntasks = (int64_t)a.node_count * (a.Bp / (32 * V));
+    if (ntasks == 0) return LDPC_OK;
+    TMap tm_msg, tm_p;
+    int rc = make_row_map(a.msg, a.msg_rows, a.Bp, V, &tm_msg);
+    if (rc == LDPC_OK) rc = make_row_map(a.P, a.p_rows, a.Bp, V, &tm_p);
+    if (rc) return rc;
+    const int64_t need = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int64_t blocks = std::min<int64_t>(need, (int64_t)per_sm * sms);
+    kern<<<(unsigned)blocks, kThreads, smem, st>>>(a, ntasks, tm_msg, tm_p);
+    LDPC_CHECK_LAUNCH();
+    return LDPC_OK;
+}
+
+// LDPC_KERNEL=tma: variable buckets of the ring path through the TMA ring (A/B of the data mover)
+bool use_tma_ring() {
+    static const bool on = [] {
+        const char *e = getenv("LDPC_KERNEL");
+        return e && std::string(e) == "tma";
+    }();
+    return on;
+}
+
 // variables get a fixed-iteration instantiation without the early-stop bookkeeping; checks
 // (ring only on request) keep the one that handles both modes
 template <int D, int V, bool IS_VAR, bool FLAG, int MINB>
 int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
     if constexpr (IS_VAR) {
+        if (use_tma_ring() && a.Bp % 64 == 0)
+            return a.done == nullptr ? launch_var_tma_ve<D, V, FLAG, MINB, false>(a, st)
+                                     : launch_var_tma_ve<D, V, FLAG, MINB, true>(a, st);
         if (a.done == nullptr) return launch_ring_ve<D, V, IS_VAR, FLAG, MINB, false>(a, st);
     }
     return launch_ring_ve<D, V, IS_VAR, FLAG, MINB, true>(a, st);

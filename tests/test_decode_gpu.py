@@ -97,6 +97,30 @@ def test_batches_vs_oracle(cuda, code, B, ebno, iters, early):
     assert np.array_equal(res.syndromes(), z)
 
 
+def test_pinned_and_pageable_buffers_agree(cuda):
+    # pageable numpy in/out goes through the decoder's pinned staging slots (several 16 MB pieces at
+    # C3 size); pinned buffers are copied directly: identical results
+    import torch
+
+    from paper_1609_01567_b200.decoder import BatchResult
+
+    H, P = _frames("C3", 160, 2.0, seed=8)
+    T = CodeTables.from_matrix(H)
+    n, m = H.n, H.m
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory().numpy()  # noqa: E731
+    P_pin = pin(P.shape, torch.float64)
+    P_pin[:] = P
+    with ParallelDecoder(T, max_batch=160, sub_batch=64) as dec:
+        pageable = dec.decode_priors(P, 6, early_stop=False)
+        out = BatchResult(pin((160, (n + 31) // 32), torch.int32).view(np.uint32), pin((160,), torch.uint8),
+                          pin((160,), torch.int32), pin((160, (m + 31) // 32), torch.int32).view(np.uint32), n, m)
+        pinned = dec.decode_priors(P_pin, 6, early_stop=False, out=out)
+        mixed = dec.decode_priors(P_pin, 6, early_stop=False)  # pinned in, pageable out
+    for r in (pinned, mixed):
+        assert np.array_equal(r.est_bits, pageable.est_bits) and np.array_equal(r.syn_bits, pageable.syn_bits)
+        assert np.array_equal(r.success, pageable.success) and np.array_equal(r.iterations, pageable.iterations)
+
+
 def test_device_path_equals_host_path(cuda):
     import torch
 
