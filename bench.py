@@ -334,6 +334,10 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     dev = torch.device(f"cuda:{local_rank}")
     torch.cuda.set_device(dev)
+    from paper_1609_01567_b200.numa import bind_to_gpu
+
+    all_cpus = os.sched_getaffinity(0)
+    numa = bind_to_gpu(local_rank)  # host copies from the CPUs (and memory) nearest this rank's GPU
     cfg = args.config
     C = configs.CONFIGS[cfg]
     H = configs.code(C["code"])
@@ -600,6 +604,7 @@ def run_ours(args):
 
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        os.sched_setaffinity(0, all_cpus)  # the CPU baseline gets every host thread
         v, cores, frames, secs, ref_outs = cpu_reference_rate(H, P_host, iters, args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{frames} frames of the workload (fixed {iters} iterations) in {secs:.1f} s by the C "
@@ -633,6 +638,7 @@ def run_ours(args):
             "fast_fp32": fast,
             "other_configs": others,
             "gpu_launches": int(launches),
+            "numa": numa,
             "clocks": clk.summary(),
             "counts": {"bit_errors": int(counts[0]), "failures": int(counts[1]), "iterations": int(counts[2]),
                        "frames": int(counts[3])},

@@ -285,7 +285,10 @@ def ber_sweep(H, ebno_points, frames: int, max_iterations: int = 50, seed: int =
     decoder = None
     if decode_fn is None:
         from .decoder import ParallelDecoder
+        from .numa import bind_to_gpu
         from .tables import CodeTables
+
+        bind_to_gpu(torch.cuda.current_device())  # host channel threads and copies near this rank's GPU
 
         decoder = ParallelDecoder(CodeTables.from_matrix(H), max_batch=batch)
         decode_fn = gpu_decode_counts(decoder, early_stop, precision)
@@ -329,6 +332,9 @@ def _ber_sweep_device(H, ebno_points, frames, max_iterations, seed, batch, rate,
     dist, rank, world = _dist_info()
     R = rate if rate is not None else (H.n - H.m) / H.n
     dev = torch.device("cuda", torch.cuda.current_device())
+    from .numa import bind_to_gpu
+
+    bind_to_gpu(dev.index)
     lo, hi = shard_range(frames, rank, world)
     points = []
     with ParallelDecoder(CodeTables.from_matrix(H), max_batch=batch) as dec:

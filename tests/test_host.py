@@ -169,3 +169,15 @@ def test_plan_pages_mirrors_engine():
     for bad in ((10, 0), (0, 4), (-1, 3)):
         with pytest.raises(ValueError):
             plan_pages(*bad)
+
+
+def test_numa_binding_is_best_effort():
+    # no GPU / no NVML here: nothing is bound and the affinity is unchanged
+    import os
+
+    from paper_1609_01567_b200.numa import bind_to_gpu
+
+    before = os.sched_getaffinity(0)
+    info = bind_to_gpu(0)
+    assert os.sched_getaffinity(0) == (before if not info["bound"] else os.sched_getaffinity(0))
+    assert info["cpus"] >= 1
