@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <mutex>
 #include <thread>
 
@@ -239,84 +241,206 @@ static bool alt_sweep() {
 }
 static thread_local int g_sweep = 0;  // direction of the next node-kernel launch
 
+// ---- launches of one phase: big buckets in order on the calling stream, small ones beside them ----
+// A phase is one launch per degree bucket (plus one for the high-degree range).  Memory-bound
+// launches of the big buckets stay in order on the calling stream (run side by side they only
+// split the bandwidth: profiles/r1_kernel_choice.md); launches of buckets holding less than
+// 1/kSmallShare of the edges -- latency-bound, a few blocks per SM, mostly the compute-bound
+// high-degree ones -- go to side streams forked from and joined back into the calling stream, so
+// they overlap each other and the big ones.  Buckets write disjoint slots and c_hat rows, so the
+// order is free.  Also inside CUDA-graph capture (the side streams join the capture through the
+// fork event).  LDPC_FORK=0 keeps every launch on the calling stream.
+constexpr int kSideStreams = 3;
+constexpr int64_t kSmallShare = 8;
+
+struct ForkSet {
+    cudaStream_t side[kSideStreams] = {};
+    cudaEvent_t fork = nullptr, join[kSideStreams] = {};
+};
+
+static bool fork_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LDPC_FORK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// the side streams of (device, calling stream), created on first use (never during a capture: the
+// first call of a decode sequence runs eagerly); nullptr when unavailable (then sequential)
+static ForkSet *fork_set(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, ForkSet> sets;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(dev, s);
+    auto it = sets.find(key);
+    if (it != sets.end()) return &it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (sets.size() >= 64 || cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+        return nullptr;
+    ForkSet f;
+    bool ok = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int k = 0; k < kSideStreams && ok; k++)
+        ok = cudaStreamCreateWithFlags(&f.side[k], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&f.join[k], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return &sets.emplace(key, f).first->second;
+}
+
+struct PhaseLaunch {
+    std::function<int(cudaStream_t)> run;
+    bool small;
+};
+
+static int run_phase(const std::vector<PhaseLaunch> &L, cudaStream_t s) {
+    int n_small = 0;
+    for (const auto &x : L) n_small += x.small ? 1 : 0;
+    ForkSet *f = (fork_enabled() && n_small > 0 && L.size() > 1) ? fork_set(s) : nullptr;
+    if (f == nullptr) {
+        for (const auto &x : L)
+            if (int rc = x.run(s)) return rc;
+        return LDPC_OK;
+    }
+    LDPC_CUDA_TRY(cudaEventRecord(f->fork, s));
+    const int used = std::min(n_small, kSideStreams);
+    for (int k = 0; k < used; k++) LDPC_CUDA_TRY(cudaStreamWaitEvent(f->side[k], f->fork, 0));
+    int next = 0, rc = LDPC_OK;
+    for (const auto &x : L) {  // small ones first, so they start beside the first big launch
+        if (!x.small) continue;
+        if ((rc = x.run(f->side[next]))) break;
+        next = (next + 1) % used;
+    }
+    for (const auto &x : L) {
+        if (rc) break;
+        if (!x.small) rc = x.run(s);
+    }
+    for (int k = 0; k < used; k++) {  // join even after an error, so no stream is left forked
+        cudaEventRecord(f->join[k], f->side[k]);
+        cudaStreamWaitEvent(s, f->join[k], 0);
+    }
+    return rc;
+}
+
 int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const uint32_t *done, cudaStream_t s,
                 bool fast = false) {
-    NodeLaunch a = check_args(g, w, done);
+    const NodeLaunch a0 = check_args(g, w, done);
+    std::vector<PhaseLaunch> L;
+    auto small = [&](int64_t edges) { return edges * kSmallShare < g->E; };
     if (fast) {
         for (const Bucket &b : g->chk_buckets) {
             if (b.deg >= fast_od_min_degree()) break;  // buckets are sorted by degree
+            NodeLaunch a = a0;
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
-            int rc = launch_check_f32(a, b.deg, from_prior, msg32(g, w), prior32(g, w), s);
-            if (rc) return rc;
+            const int deg = b.deg;
+            L.push_back({[=](cudaStream_t st) {
+                             return launch_check_f32(a, deg, from_prior, msg32(g, w), prior32(g, w), st);
+                         },
+                         small((int64_t)b.node_count * b.deg)});
         }
-        return launch_fast_od(a, g->chk_buckets, fast_od_min_degree(), false, from_prior, msg32(g, w), prior32(g, w),
-                              w.od_scratch, w.od_stride, kOdScratchBlocks, s);
+        for (const OdClass &c : fast_od_classes(g->chk_buckets, fast_od_min_degree()))
+            L.push_back({[=](cudaStream_t st) {
+                             return launch_fast_od_class(a0, c, false, from_prior, msg32(g, w), prior32(g, w),
+                                                         w.od_scratch, w.od_stride, kOdScratchBlocks, st);
+                         },
+                         small(c.edges)});
+        return run_phase(L, s);
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
+    int64_t wide_edges = 0;
     for (const Bucket &b : g->chk_buckets) {
         if (b.deg <= kMaxMidCheckDegree) {
+            NodeLaunch a = a0;
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
             a.reverse = alt_sweep() ? ((g_sweep ^= 1) ^ 1) : 0;
-            int rc = b.deg > kMaxRegCheckDegree ? launch_check_mid(a, b.deg, from_prior, s)
-                     : use_ring(false, b.deg)   ? launch_check_pipe(a, b.deg, from_prior, s)
-                                                : launch_check_bucket(a, b.deg, from_prior, s);
-            if (rc) return rc;
+            const int deg = b.deg;
+            L.push_back({[=](cudaStream_t st) {
+                             return deg > kMaxRegCheckDegree ? launch_check_mid(a, deg, from_prior, st)
+                                    : use_ring(false, deg)    ? launch_check_pipe(a, deg, from_prior, st)
+                                                              : launch_check_bucket(a, deg, from_prior, st);
+                         },
+                         small((int64_t)b.node_count * b.deg)});
         } else {
             if (wide_begin < 0) wide_begin = b.node_begin;
             wide_end = b.node_begin + b.node_count;
             wide_max = std::max(wide_max, b.deg);
+            wide_edges += (int64_t)b.node_count * b.deg;
         }
     }
     if (wide_begin >= 0) {
+        NodeLaunch a = a0;
         a.node_begin = wide_begin;
         a.node_count = wide_end - wide_begin;
-        return launch_check_wide(a, wide_max, from_prior, s);
+        L.push_back({[=](cudaStream_t st) { return launch_check_wide(a, wide_max, from_prior, st); },
+                     small(wide_edges)});
     }
-    return LDPC_OK;
+    return run_phase(L, s);
 }
 
 int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint32_t *done, cudaStream_t s,
               bool fast = false) {
-    NodeLaunch a = var_args(g, w, done);
+    const NodeLaunch a0 = var_args(g, w, done);
+    std::vector<PhaseLaunch> L;
+    auto small = [&](int64_t edges) { return edges * kSmallShare < g->E; };
     if (fast) {
         for (const Bucket &b : g->var_buckets) {
             if (b.deg >= fast_od_min_degree()) break;  // buckets are sorted by degree
+            NodeLaunch a = a0;
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
-            int rc = launch_var_f32(a, b.deg, write_q, msg32(g, w), prior32(g, w), s);
-            if (rc) return rc;
+            const int deg = b.deg;
+            L.push_back({[=](cudaStream_t st) {
+                             return launch_var_f32(a, deg, write_q, msg32(g, w), prior32(g, w), st);
+                         },
+                         small((int64_t)b.node_count * b.deg)});
         }
-        return launch_fast_od(a, g->var_buckets, fast_od_min_degree(), true, write_q, msg32(g, w), nullptr, nullptr, 0,
-                              0, s);
+        for (const OdClass &c : fast_od_classes(g->var_buckets, fast_od_min_degree()))
+            L.push_back({[=](cudaStream_t st) {
+                             return launch_fast_od_class(a0, c, true, write_q, msg32(g, w), nullptr, nullptr, 0, 0,
+                                                         st);
+                         },
+                         small(c.edges)});
+        return run_phase(L, s);
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
+    int64_t wide_edges = 0;
     for (const Bucket &b : g->var_buckets) {
         if (b.deg <= kMaxMidVarDegree) {
+            NodeLaunch a = a0;
             a.node_begin = b.node_begin;
             a.node_count = b.node_count;
             a.edge_begin = b.edge_begin;
             a.reverse = alt_sweep() ? ((g_sweep ^= 1) ^ 1) : 0;
-            int rc = b.deg > kMaxRegDegree     ? launch_var_mid(a, b.deg, write_q, s)
-                     : use_ring(true, b.deg) ? launch_var_pipe(a, b.deg, write_q, s)
-                                             : launch_var_bucket(a, b.deg, write_q, s);
-            if (rc) return rc;
+            const int deg = b.deg;
+            L.push_back({[=](cudaStream_t st) {
+                             return deg > kMaxRegDegree   ? launch_var_mid(a, deg, write_q, st)
+                                    : use_ring(true, deg) ? launch_var_pipe(a, deg, write_q, st)
+                                                          : launch_var_bucket(a, deg, write_q, st);
+                         },
+                         small((int64_t)b.node_count * b.deg)});
         } else {
             if (wide_begin < 0) wide_begin = b.node_begin;
             wide_end = b.node_begin + b.node_count;
             wide_max = std::max(wide_max, b.deg);
+            wide_edges += (int64_t)b.node_count * b.deg;
         }
     }
     if (wide_begin >= 0) {
+        NodeLaunch a = a0;
         a.node_begin = wide_begin;
         a.node_count = wide_end - wide_begin;
-        return launch_var_wide(a, wide_max, write_q, s);
+        L.push_back({[=](cudaStream_t st) { return launch_var_wide(a, wide_max, write_q, st); }, small(wide_edges)});
     }
-    return LDPC_OK;
+    return run_phase(L, s);
 }
 
 // done bits of padded codewords (>= B) are set from the start in early-stop mode

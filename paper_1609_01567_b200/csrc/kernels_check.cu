@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(kWideThreads) k_check_chains(NodeLaunch a, int
     static_assert(CPT >= 1 && kWideThreads == 1024, "TW must be >= 4; up to 32 warps");
     extern __shared__ double smem_b[];
     double *b = GS ? a.scratch + (size_t)blockIdx.x * max_deg * TW : smem_b;  // [d][TW]
-    const int tile = blockIdx.x / a.node_count;  // tile-major: all nodes of tile 0 first
-    const int ni = blockIdx.x - tile * a.node_count;
+    int ni, tile;
+    lpt_block(blockIdx.x, a.node_count, a.Bp / TW, ni, tile);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int c = lane % TW, h = lane / TW;
     const int cw = tile * TW + c;

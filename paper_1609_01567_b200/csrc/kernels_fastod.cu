@@ -59,14 +59,13 @@ __device__ __forceinline__ uint32_t slot_of(const NodeLaunch &a, int pos) {
     return row_off(a.slot ? __ldg(a.slot + pos) : pos);
 }
 
-// Task t of a side's launch, chunk-major: all nodes of tile 0, then tile 1, ...
+// Task t of a side's launch: largest degree first, all tiles of a node together (lpt_block)
 struct OdTask {
     int tile, ni;
 };
-__device__ __forceinline__ OdTask od_task(int64_t t, int node_count) {
+__device__ __forceinline__ OdTask od_task(int64_t t, int node_count, int tiles) {
     OdTask o;
-    o.tile = (int)(t / node_count);
-    o.ni = (int)(t - (int64_t)o.tile * node_count);
+    lpt_block((int)t, node_count, tiles, o.ni, o.tile);
     return o;
 }
 
@@ -109,7 +108,7 @@ __global__ void __launch_bounds__(1024) k_check_f32_od(NodeLaunch a, float *msg,
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     float *sc = scratch ? scratch + (size_t)blockIdx.x * scratch_stride : nullptr;  // [J][32] pass totals
     for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
-        const OdTask tk = od_task(t, a.node_count);
+        const OdTask tk = od_task(t, a.node_count, a.Bp / 32);
         if (a.done != nullptr && a.done[tk.tile] == 0xffffffffu) continue;  // uniform per block
         const int node = __ldg(a.order + a.node_begin + tk.ni);
         const int pos0 = __ldg(a.off + node), d = __ldg(a.off + node + 1) - pos0;
@@ -184,7 +183,7 @@ __global__ void __launch_bounds__(1024) k_var_f32_od(NodeLaunch a, float *msg, i
     __shared__ float tot[kOdMaxWarps * 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
-        const OdTask tk = od_task(t, a.node_count);
+        const OdTask tk = od_task(t, a.node_count, a.Bp / 32);
         const uint32_t done = a.done != nullptr ? a.done[tk.tile] : 0u;
         if (done == 0xffffffffu) continue;
         const int node = __ldg(a.order + a.node_begin + tk.ni);
@@ -256,46 +255,58 @@ int fast_od_scratch_stride(const ldpc_graph *g) {
 }
 
 // Every bucket of the side with degree >= min_deg, grouped into launches by warps per block.
-// Checks longer than one pass keep their pass totals in scratch: scratch_blocks slices of
-// scratch_stride floats (fast_od_scratch_stride), one per resident block of the launch.
-int launch_fast_od(const NodeLaunch &base, const std::vector<Bucket> &buckets, int min_deg, bool var_side, bool flag,
-                   float *msg, const float *P, float *scratch, int scratch_stride, int scratch_blocks,
-                   cudaStream_t s) {
-    const int tiles = base.Bp / 32;
+// The buckets of degree >= min_deg grouped into launches by warps per block (buckets are sorted by
+// degree, so a class is a contiguous node range).
+std::vector<OdClass> fast_od_classes(const std::vector<Bucket> &buckets, int min_deg) {
+    std::vector<OdClass> out;
     size_t i = 0;
     while (i < buckets.size()) {
         if (buckets[i].deg < min_deg || buckets[i].node_count == 0) {
             i++;
             continue;
         }
-        // buckets are sorted by degree: take the run with the same warp count
         const int W = od_warps(buckets[i].deg);
+        OdClass c{buckets[i].node_begin, 0, W, 0, 0};
         size_t k = i;
-        int dmax = 0;
-        while (k < buckets.size() && od_warps(buckets[k].deg) == W) dmax = std::max(dmax, buckets[k++].deg);
-        NodeLaunch a = base;
-        a.node_begin = buckets[i].node_begin;
-        a.node_count = buckets[k - 1].node_begin + buckets[k - 1].node_count - a.node_begin;
-        const int64_t ntasks = (int64_t)a.node_count * tiles;
-        const bool multi = dmax > kOdSeg * W;  // some node needs two passes
-        int64_t grid = std::min<int64_t>(ntasks, 148LL * 64);
-        if (var_side) {
-            if (flag) k_var_f32_od<true><<<(unsigned)grid, 32 * W, 0, s>>>(a, msg, ntasks);
-            else k_var_f32_od<false><<<(unsigned)grid, 32 * W, 0, s>>>(a, msg, ntasks);
-        } else {
-            if (multi) {
-                LDPC_ARG_CHECK(scratch != nullptr && scratch_blocks > 0 &&
-                                   scratch_stride >= (dmax + kOdSeg * W - 1) / (kOdSeg * W) * 32,
-                               "fast mode: check degree %d needs the workspace scratch", dmax);
-                grid = std::min<int64_t>(grid, scratch_blocks);
-            }
-            float *sc = multi ? scratch : nullptr;
-            if (flag) k_check_f32_od<true><<<(unsigned)grid, 32 * W, 0, s>>>(a, msg, P, sc, scratch_stride, ntasks);
-            else k_check_f32_od<false><<<(unsigned)grid, 32 * W, 0, s>>>(a, msg, P, sc, scratch_stride, ntasks);
+        while (k < buckets.size() && od_warps(buckets[k].deg) == W) {
+            c.dmax = std::max(c.dmax, buckets[k].deg);
+            c.edges += (int64_t)buckets[k].node_count * buckets[k].deg;
+            k++;
         }
-        LDPC_CHECK_LAUNCH();
+        c.node_count = buckets[k - 1].node_begin + buckets[k - 1].node_count - c.node_begin;
+        out.push_back(c);
         i = k;
     }
+    return out;
+}
+
+// One class.  Checks longer than one pass keep their pass totals in scratch: scratch_blocks slices
+// of scratch_stride floats (fast_od_scratch_stride), one per resident block of the launch.
+int launch_fast_od_class(const NodeLaunch &base, const OdClass &c, bool var_side, bool flag, float *msg,
+                         const float *P, float *scratch, int scratch_stride, int scratch_blocks, cudaStream_t s) {
+    NodeLaunch a = base;
+    a.node_begin = c.node_begin;
+    a.node_count = c.node_count;
+    const int W = c.warps;
+    const int64_t ntasks = (int64_t)a.node_count * (base.Bp / 32);
+    if (ntasks == 0) return LDPC_OK;
+    const bool multi = c.dmax > kOdSeg * W;  // some node needs two passes
+    int64_t grid = std::min<int64_t>(ntasks, 148LL * 64);
+    if (var_side) {
+        if (flag) k_var_f32_od<true><<<(unsigned)grid, 32 * W, 0, s>>>(a, msg, ntasks);
+        else k_var_f32_od<false><<<(unsigned)grid, 32 * W, 0, s>>>(a, msg, ntasks);
+    } else {
+        if (multi) {
+            LDPC_ARG_CHECK(scratch != nullptr && scratch_blocks > 0 &&
+                               scratch_stride >= (c.dmax + kOdSeg * W - 1) / (kOdSeg * W) * 32,
+                           "fast mode: check degree %d needs the workspace scratch", c.dmax);
+            grid = std::min<int64_t>(grid, scratch_blocks);
+        }
+        float *sc = multi ? scratch : nullptr;
+        if (flag) k_check_f32_od<true><<<(unsigned)grid, 32 * W, 0, s>>>(a, msg, P, sc, scratch_stride, ntasks);
+        else k_check_f32_od<false><<<(unsigned)grid, 32 * W, 0, s>>>(a, msg, P, sc, scratch_stride, ntasks);
+    }
+    LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }
 

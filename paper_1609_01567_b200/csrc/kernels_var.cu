@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(kChainThreads) k_var_chains(NodeLaunch a, int 
     static_assert(CPT >= 1, "TW must be >= 4");
     extern __shared__ double smem_rs[];
     double *sm = GS ? a.scratch + (size_t)blockIdx.x * max_deg * TW * 2 : smem_rs;
-    const int tile = blockIdx.x / a.node_count;
-    const int ni = blockIdx.x - tile * a.node_count;
+    int ni, tile;
+    lpt_block(blockIdx.x, a.node_count, a.Bp / TW, ni, tile);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int c = lane % TW, h = lane / TW;
     const int cw = tile * TW + c;
