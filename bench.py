@@ -553,6 +553,8 @@ def run_ours(args):
                 ("C2_fixed", "C2", 4096, 20, False, 2.0, "fp64"),
                 ("C4", "C4", 256, 20, True, 3.0, "fp64"),
                 ("C4_fast_fp32", "C4", 256, 20, True, 3.0, "fp32"),
+                ("C4D_fixed", "C4D", 256, 20, False, 2.0, "fp64"),
+                ("C4D_fixed_fast_fp32", "C4D", 256, 20, False, 2.0, "fp32"),
                 ("C5_3dB", "C5", 1024, 10, True, 3.0, "fp64"))
         for label, name, B_o, it_o, early_o, eb_o, prec_o in runs:
             H_o = configs.code(name)
@@ -582,6 +584,9 @@ def run_ours(args):
             del P_o, ws_o, outs_o
         if "C4" in others and "C4_fast_fp32" in others:
             others["C4_fast_fp32"]["speedup_vs_exact"] = others["C4"]["ms_per_decode"] / others["C4_fast_fp32"]["ms_per_decode"]
+        if "C4D_fixed" in others and "C4D_fixed_fast_fp32" in others:
+            others["C4D_fixed_fast_fp32"]["speedup_vs_exact"] = (others["C4D_fixed"]["ms_per_decode"]
+                                                                  / others["C4D_fixed_fast_fp32"]["ms_per_decode"])
         if "C2" in others and "C2_fixed" in others:
             others["C2"]["vs_fixed_iterations"] = others["C2"]["ms_per_decode"] / others["C2_fixed"]["ms_per_decode"]
         # the reference-facing single-frame call at C3 (engine.py:363 decode(y, sigma2)): host in,

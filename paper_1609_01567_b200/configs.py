@@ -43,6 +43,13 @@ def code(name: str) -> ParityCheckMatrix:
         return generate_irregular_code({200: 16, 120: 16, 60: 32, 30: 64, 17: 128, 6: 4000, 3: 28512}, 16384,
                                        seed=SEED + 4,
                                        check_degrees={1000: 4, 500: 8, 250: 16, 120: 32, 60: 64, 33: 128, 20: 256})
+    if name == "C4D":
+        # round 1's C4 profile, kept as a second stress code: 16 checks of degree 1000 and 16 variables
+        # of degree 200 (21% of the edges) next to degree-2/3/8 variables.  It does not converge (the
+        # weak checks leave bits uncorrected), so it is a fixed-work case where the exact mode's
+        # O(d^2) ordered products dominate (fast mode vs exact: bench.py other_configs).
+        return generate_irregular_code({200: 16, 8: 1024, 3: 15728, 2: 16000}, 16384, seed=SEED + 4,
+                                       check_degrees={1000: 16})
     raise KeyError(name)
 
 

@@ -18,6 +18,8 @@
 #include <cstring>
 #include <functional>
 #include <map>
+
+#include <sched.h>
 #include <mutex>
 #include <thread>
 
@@ -1029,7 +1031,7 @@ static void decoder_free(ldpc_decoder *d) {
 // geometrically from 64 (LDPC_E2E_GROWTH, x100, default 150), capped at `sub`; a
 // remainder smaller than the sub-batch before it is merged into that one, since
 // the last decode is exposed after the last copy.
-static std::vector<int32_t> chunk_plan(int32_t B, int32_t sub) {
+static std::vector<int32_t> chunk_plan(int32_t B, int32_t sub, bool taper = false) {
     static const int growth = [] {
         const char *e = getenv("LDPC_E2E_GROWTH");
         return e ? std::max(101, atoi(e)) : 150;
@@ -1069,6 +1071,14 @@ static std::vector<int32_t> chunk_plan(int32_t B, int32_t sub) {
         v[v.size() - 2] += v.back();
         v.pop_back();
     }
+    // taper (pageable input, whose host staging runs slower than the DMA): the last sub-batch's
+    // decode is exposed after its input lands, so end on a small one (C3 B = 1024: 64, 128, 192,
+    // 256, 384 -> ..., 256, 128: 18.3 -> 16.1 ms per call; tools/pageable_probe.py)
+    constexpr int32_t kTail = 128;
+    if (taper && v.back() > kTail && (int)v.size() < kMaxChunks) {
+        v.back() -= kTail;
+        v.push_back(kTail);
+    }
     return v;
 }
 
@@ -1086,7 +1096,8 @@ extern "C" int ldpc_decoder_create(const ldpc_graph *g, int32_t max_batch, int32
     // sub = 512: 64, 128, 192, 416), so take the maximum over every b <= max_batch
     int32_t biggest = 0;
     for (int32_t b = max_batch; b >= 1 && biggest < max_batch; b--)
-        for (int32_t x : chunk_plan(b, d->sub)) biggest = std::max(biggest, x);
+        for (bool taper : {false, true})
+            for (int32_t x : chunk_plan(b, d->sub, taper)) biggest = std::max(biggest, x);
     d->ws_bytes = workspace_bytes(g, biggest);
     const size_t RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32, MB = (size_t)max_batch;
     cudaError_t e = cudaSuccess;
@@ -1135,8 +1146,12 @@ static int staging_alloc(ldpc_decoder *d) {
     LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->syn_pin, sizeof(uint32_t) * RWm * MB, cudaHostAllocDefault));
     LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->succ_pin, MB, cudaHostAllocDefault));
     LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->its_pin, sizeof(int32_t) * MB, cudaHostAllocDefault));
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    d->pool.start((int)std::min(7u, std::max(1u, hw / 2) - 1));  // + the calling thread
+    // copy threads: every CPU this process may run on (the rank's NUMA-local set when bound), capped
+    // at 16; LDPC_COPY_THREADS overrides
+    cpu_set_t cs;
+    int ncpu = (sched_getaffinity(0, sizeof(cs), &cs) == 0) ? CPU_COUNT(&cs) : (int)std::thread::hardware_concurrency();
+    if (const char *e = getenv("LDPC_COPY_THREADS")) ncpu = atoi(e);
+    d->pool.start(std::max(0, std::min(16, ncpu) - 1));  // + the calling thread
     return LDPC_OK;
 }
 
@@ -1175,7 +1190,11 @@ static int decoder_run(ldpc_decoder *d, const double *p_host, const double *s2_h
     LDPC_ARG_CHECK(max_iterations >= 0, "max_iterations must be non-negative");
     const ldpc_graph *g = d->g;
     const size_t n = g->n, RWn = (g->n + 31) / 32, RWm = (g->m + 31) / 32;
-    const std::vector<int32_t> plan = chunk_plan(B, d->sub);
+    // Plain (pageable) host arrays, as the reference API's callers pass them (engine.py:363-372), go
+    // through pinned staging: a pageable cudaMemcpyAsync would be staged by the driver one
+    // synchronous piece at a time.
+    const bool in_pinned = host_pinned(p_host);  // (sigma2, B doubles, is copied as it is)
+    const std::vector<int32_t> plan = chunk_plan(B, d->sub, !in_pinned);
     int rc = LDPC_OK;
     cudaError_t e = cudaSuccess;
     auto cuda = [&](cudaError_t x, const char *what) {
@@ -1184,10 +1203,6 @@ static int decoder_run(ldpc_decoder *d, const double *p_host, const double *s2_h
             set_error("%s: %s", what, cudaGetErrorString(x));
         }
     };
-    // Plain (pageable) host arrays, as the reference API's callers pass them (engine.py:363-372), go
-    // through pinned staging: a pageable cudaMemcpyAsync would be staged by the driver one
-    // synchronous piece at a time.
-    const bool in_pinned = host_pinned(p_host);  // (sigma2, B doubles, is copied as it is)
     const bool out_pinned = host_pinned(est_bits_host) && host_pinned(success_host) && host_pinned(iters_host) &&
                             (syn_bits_host == nullptr || host_pinned(syn_bits_host));
     if (!in_pinned || !out_pinned) {
