@@ -144,13 +144,14 @@ __device__ __forceinline__ void move_row(T *a, int32_t rows, int32_t r, const in
 __global__ void k_compact_apply(const uint32_t *__restrict__ chat, int32_t n, int32_t NWs,
                                 const uint32_t *__restrict__ ret_sel, const int32_t *__restrict__ ret_orig,
                                 const int32_t *__restrict__ iters_ws, const int32_t *__restrict__ ctl, DecodeOut out,
-                                int32_t RWm, int32_t B, const int32_t *__restrict__ perm, MoveArrays arr) {
+                                int32_t RWm, int32_t B, const int32_t *__restrict__ perm, MoveArrays arr,
+                                int retire) {
     if (ctl[1] == 0) return;
     const int lane = threadIdx.x & 31;
     const int NWa = 2 * ctl[4];  // the words active before the plan: ret_sel / ret_orig cover exactly those
     const int L = ctl[2], oc0 = ctl[3], new_act = ctl[0];
     const int RWn = (n + 31) / 32;
-    const int64_t T0 = (int64_t)RWn * NWa, T1 = NWa;
+    const int64_t T0 = retire ? (int64_t)RWn * NWa : 0, T1 = retire ? NWa : 0;
     int64_t total = T0 + T1;
     for (int i = 0; i < arr.count; i++) total += arr.rows[i];
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -248,25 +249,42 @@ int launch_compact_init(const Workspace &w, cudaStream_t s) {
     return LDPC_OK;
 }
 
-// One compaction point (after the syndrome of a round): the early-stop update and the plan, then one launch that
-// retires the stopped codewords and moves the rows of the state arrays (msg, priors, ...).
+// One compaction point (after the syndrome of a round): the early-stop update and the plan on `s`;
+// then the message rows move on `s` (the next check phase reads them) while the retiring of the
+// stopped codewords and the other state arrays (priors, read by the next variable phase) move on
+// `side` when given (the caller joins it back before that variable phase), else on `s`.
 int launch_compact(const ldpc_graph *g, const Workspace &w, int32_t round, int frac_pct, const DecodeOut &out,
-                   const CompactArray *arrays, int count, cudaStream_t s) {
+                   const CompactArray *arrays, int count, cudaStream_t s, cudaStream_t side,
+                   cudaEvent_t fork) {
     LDPC_ARG_CHECK(count >= 1 && count <= 3, "compaction moves 1..3 arrays");
     k_compact_plan<<<1, kPlanThreads, 0, s>>>(w.done, w.unsat, w.iters, w.NW, round, w.orig, w.ret_orig, w.perm,
                                               w.ret_sel, w.ctl, frac_pct);
     LDPC_CHECK_LAUNCH();
-    MoveArrays arr{};
-    int64_t rows = 0;
-    for (int i = 0; i < count; i++) {
-        arr.p[i] = arrays[i].p;
-        arr.rows[i] = arrays[i].rows;
-        arr.elem[i] = arrays[i].elem_bytes;
-        rows += arrays[i].rows;
+    MoveArrays first{}, rest{};
+    first.p[0] = arrays[0].p;
+    first.rows[0] = arrays[0].rows;
+    first.elem[0] = arrays[0].elem_bytes;
+    first.count = 1;
+    int64_t rows_rest = 0;
+    for (int i = 1; i < count; i++) {
+        rest.p[i - 1] = arrays[i].p;
+        rest.rows[i - 1] = arrays[i].rows;
+        rest.elem[i - 1] = arrays[i].elem_bytes;
+        rows_rest += arrays[i].rows;
     }
-    arr.count = count;
-    k_compact_apply<<<blocks_of(32 * rows, 256, 148 * 32), 256, 0, s>>>(
-        w.chat, g->n, w.NWs, w.ret_sel, w.ret_orig, w.iters, w.ctl, out, (g->m + 31) / 32, w.B, w.perm, arr);
+    rest.count = count - 1;
+    cudaStream_t s2 = s;
+    if (side != nullptr) {
+        LDPC_CUDA_TRY(cudaEventRecord(fork, s));
+        LDPC_CUDA_TRY(cudaStreamWaitEvent(side, fork, 0));
+        s2 = side;
+    }
+    const int64_t tiles = (int64_t)((g->n + 31) / 32) * w.NW;
+    k_compact_apply<<<blocks_of(32 * std::max<int64_t>(rows_rest, tiles), 256, 148 * 32), 256, 0, s2>>>(
+        w.chat, g->n, w.NWs, w.ret_sel, w.ret_orig, w.iters, w.ctl, out, (g->m + 31) / 32, w.B, w.perm, rest, 1);
+    LDPC_CHECK_LAUNCH();
+    k_compact_apply<<<blocks_of(32 * (int64_t)arrays[0].rows, 256, 148 * 32), 256, 0, s>>>(
+        w.chat, g->n, w.NWs, w.ret_sel, w.ret_orig, w.iters, w.ctl, out, (g->m + 31) / 32, w.B, w.perm, first, 0);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }

@@ -470,6 +470,35 @@ int init_flags(const Workspace &w, bool early, cudaStream_t s, int32_t chat_rows
 
 }  // namespace
 
+// The compaction's side stream of (device, calling stream): its own stream and events, apart from the
+// phase side streams (created eagerly like those; nullptr during a capture that has none yet)
+struct CompactFork {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static CompactFork *compact_fork(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, CompactFork> sets;
+    if (!fork_enabled()) return nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(dev, s);
+    auto it = sets.find(key);
+    if (it != sets.end()) return &it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (sets.size() >= 64 || cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+        return nullptr;
+    CompactFork f;
+    if (cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return &sets.emplace(key, f).first->second;
+}
+
 // Early-stop compaction (compact.cu): compact when the live codewords fit in at most this percent
 // of the active chunks; LDPC_COMPACT=0 disables it, LDPC_COMPACT=<pct> sets the threshold.
 static int compact_pct() {
@@ -493,6 +522,7 @@ static int decode_view(const ldpc_graph *g, const Workspace &w, int32_t max_iter
     const int64_t e_bytes = (wb * E + wb * n + n / 8) * B;   // read r, p; write c_hat bits
     const int64_t s_bytes = (n / 8) * B;                     // read c_hat bits
     const uint32_t *done = early ? w.done : nullptr;
+    CompactFork *cf = nullptr;
     RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, true, nullptr, s, fast));
     for (int32_t t = 1; t <= max_iter; t++) {
         RUN(LDPC_KCLASS_VARIABLE, ve_bytes, var_phase(g, w, true, done, s, fast));
@@ -506,9 +536,18 @@ static int decode_view(const ldpc_graph *g, const Workspace &w, int32_t max_iter
             // variable kernels read)
             const CompactArray exact[2] = {{w.msg, (int32_t)E, 8}, {w.P, (int32_t)n, 8}};
             const CompactArray f32[3] = {{msg32(g, w), (int32_t)E, 4}, {prior32(g, w), (int32_t)n, 4}, {w.P, (int32_t)n, 8}};
-            RUN(LDPC_KCLASS_LAYOUT, 0, launch_compact(g, w, t - 1, compact_pct(), *out, fast ? f32 : exact, fast ? 3 : 2, s));
+            // the priors move and the stopped codewords retire beside the check phase (joined before
+            // the next variable phase, which reads both); eager profiling keeps one stream
+            cf = prof.out == nullptr ? compact_fork(s) : nullptr;
+            RUN(LDPC_KCLASS_LAYOUT, 0, launch_compact(g, w, t - 1, compact_pct(), *out, fast ? f32 : exact, fast ? 3 : 2, s,
+                                                      cf ? cf->side : nullptr, cf ? cf->fork : nullptr));
         }
         RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, false, done, s, fast));
+        if (cf != nullptr) {
+            LDPC_CUDA_TRY(cudaEventRecord(cf->join, cf->side));
+            LDPC_CUDA_TRY(cudaStreamWaitEvent(s, cf->join, 0));
+            cf = nullptr;
+        }
     }
     RUN(LDPC_KCLASS_ESTIMATE, e_bytes, var_phase(g, w, false, done, s, fast));
     RUN(LDPC_KCLASS_SYNDROME, s_bytes + (m / 8) * B, launch_syndrome(g, w, true, early, s));

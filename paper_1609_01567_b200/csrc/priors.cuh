@@ -17,6 +17,10 @@
 //   P = r^2 (r^2 (a6 r + a5) + (a4 r + a3)) + (a2 r + a1)
 //   e = T2[j] (P r + T1[j]) + T2[j];  exp(x) = e 2^floor(k)
 // Rare path (|x| beyond that, +-inf): SVML's scalar 64-entry-table routine.
+//
+// Attribution: the algorithm, its constants and both tables are Intel's SVML exp (__svml_exp8_ha,
+// __svml_dexp_ha_cout_rare_internal) as vendored in numpy under the BSD-3-Clause license
+// (Copyright (c) Intel Corporation; numpy/_core/src/umath/svml/LICENSE); restated here.
 #pragma once
 #include <cstdint>
 
