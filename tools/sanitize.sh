@@ -4,3 +4,9 @@ for tool in memcheck racecheck synccheck initcheck; do
       > gpurun_out/sanitize_$tool.log 2>&1
   echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_$tool.log | tail -1)"
 done
+# the TMA ring (bulk-tensor gathers into mbarrier-completed stages) under the same workload
+for tool in memcheck racecheck synccheck; do
+  LDPC_KERNEL=tma timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 python tools/sanitize_workload.py \
+      > gpurun_out/sanitize_tma_$tool.log 2>&1
+  echo "tma $tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_tma_$tool.log | tail -1)"
+done

@@ -3,7 +3,8 @@ family on tiny inputs -- graph build, streaming decode (check register kernel, v
 syndrome, done flags, layout), on-chip decode (1 CTA and a 2-CTA cluster), high-degree chains
 kernels (1024-thread and small blocks), the register check path past degree 16, fp32 fast mode,
 the phase API, the host and streaming decoders, the device channel, device priors from observations
-(fused layout kernel, on-chip, standalone exp/prior kernels)."""
+(fused layout kernel, on-chip, standalone exp/prior kernels); round 2: early-stop compaction, the
+O(d) fast-mode kernels, forked small buckets, pageable staging."""
 import sys
 
 import numpy as np
@@ -79,5 +80,22 @@ with ParallelDecoder(CodeTables.from_matrix(H6), max_batch=3) as dec:
     dec.decode_priors(P6, 4, early_stop=False, schedule="grid")
 with ParallelDecoder(CodeTables.from_matrix(H4), max_batch=2) as dec:
     dec.decode_priors(priors(H4, 2, 1.5, 10), 2, early_stop=True, schedule="stream")
+# round 2: early-stop compaction (plan, fused retire/move, mapped outputs; exact and fp32, side
+# streams), O(d) fast-mode kernels at any degree (incl. a two-pass check of degree 600), forked small
+# buckets, pageable staging through pinned slots, the TMA ring (LDPC_KERNEL=tma in a second run)
+H8 = configs.code("C2")
+with ParallelDecoder(CodeTables.from_matrix(H8), max_batch=200) as dec:
+    P8 = priors(H8, 200, 2.0, 13)
+    for prec in ("fp64", "fp32"):
+        dec.decode_priors(P8, 12, early_stop=True, precision=prec, schedule="stream")
+with ParallelDecoder(CodeTables.from_matrix(H4), max_batch=70) as dec:
+    P4 = priors(H4, 70, 2.0, 14)
+    dec.decode_priors(P4, 4, early_stop=True, precision="fp32")
+    dec.decode_priors(P4, 3, early_stop=False, precision="fp32")
+with ParallelDecoder(CodeTables.from_matrix(H5), max_batch=3) as dec:
+    dec.decode_priors(priors(H5, 3, 1.5, 15), 3, precision="fp32")
+H9 = configs.code("C3")
+with ParallelDecoder(CodeTables.from_matrix(H9), max_batch=64, sub_batch=64) as dec:
+    dec.decode_priors(priors(H9, 64, 2.0, 16), 2, early_stop=False)  # pageable in/out: staged
 torch.cuda.synchronize()
 print("sanitize workload done")
