@@ -30,4 +30,15 @@ echo "onchip capture rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_transpose_priors -s 20 -c 2 \
     -o $OUT/prof_${TAG}_priors python tools/prior_kernel_probe.py > $OUT/ncu_priors_$TAG.log 2>&1
 echo "priors capture rc=$?"
+# round 2: C4 per-kernel fp64-pipe activity and SM balance (metric list, exact and fast mode);
+# --set full of the O(d) fast-mode kernels (C4) and of the compaction kernels (C2, early stop)
+bash tools/c4_ncu.sh fp64 > $OUT/c4_fp64_$TAG.csv 2> /dev/null
+bash tools/c4_ncu.sh fp32 > $OUT/c4_fp32_$TAG.csv 2> /dev/null
+echo "c4 metric lists rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_(check|var)_f32_od" -s 10 -c 4 \
+    -o $OUT/prof_${TAG}_fastod python tools/c4_profile.py fp32 1 > $OUT/ncu_fastod_$TAG.log 2>&1
+echo "fast O(d) capture rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_compact" -s 4 -c 4 \
+    -o $OUT/prof_${TAG}_compact python tools/compact_breakdown.py C2 4096 20 2.0 > $OUT/ncu_compact_$TAG.log 2>&1
+echo "compaction capture rc=$?"
 ls -la $OUT
