@@ -582,6 +582,18 @@ def run_ours(args):
                              "mean_iterations": its_o.mean().item(), "max_iterations_used": its_o.max().item(),
                              "n": H_o.n, "edges": H_o.total_edges}
             del P_o, ws_o, outs_o
+        # fp64-pipe activity of the high-degree (O(d^2)) kernels at C4, from the committed ncu metric
+        # list of one C4 decode (a profiler number, so not measured here: profiles/ncu_c4_fp64.json)
+        try:
+            c4k = json.loads((ROOT / "profiles" / "ncu_c4_fp64.json").read_text())["kernels"]
+            chains = {k: {"fp64_pipe_pct": v["fp64_pipe_pct"], "sm_active_balance": v["sm_active_balance"],
+                          "share_of_decode": v["share"]}
+                      for k, v in c4k.items() if "chains" in k and v["launches"] > 2}
+            others["C4"]["fp64_pipe"] = {"kernels": chains, "source": "profiles/ncu_c4_fp64.json (tools/c4_ncu.sh: "
+                                         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active, "
+                                         "sm__cycles_active avg/max, one C4 decode under ncu)"}
+        except Exception:
+            pass
         if "C4" in others and "C4_fast_fp32" in others:
             others["C4_fast_fp32"]["speedup_vs_exact"] = others["C4"]["ms_per_decode"] / others["C4_fast_fp32"]["ms_per_decode"]
         if "C4D_fixed" in others and "C4D_fixed_fast_fp32" in others:
