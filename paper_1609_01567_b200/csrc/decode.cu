@@ -1175,16 +1175,21 @@ static bool host_pinned(const void *p) {
 }
 
 static int staging_alloc(ldpc_decoder *d) {
-    if (d->stage[0] != nullptr) return LDPC_OK;
+    // complete or nothing: a failed allocation is retried by the next pageable call (whatever was
+    // allocated stays owned by the decoder and is freed with it)
+    bool done = d->its_pin != nullptr;
+    for (int k = 0; k < ldpc_decoder::kStages; k++) done = done && d->stage[k] && d->stage_free[k];
+    if (done) return LDPC_OK;
     const size_t MB = (size_t)d->max_batch, RWn = (d->g->n + 31) / 32, RWm = (d->g->m + 31) / 32;
     for (int k = 0; k < ldpc_decoder::kStages; k++) {
-        LDPC_CUDA_TRY(cudaHostAlloc(&d->stage[k], ldpc_decoder::kStageBytes, cudaHostAllocDefault));
-        LDPC_CUDA_TRY(cudaEventCreateWithFlags(&d->stage_free[k], cudaEventDisableTiming));
+        if (!d->stage[k]) LDPC_CUDA_TRY(cudaHostAlloc(&d->stage[k], ldpc_decoder::kStageBytes, cudaHostAllocDefault));
+        if (!d->stage_free[k]) LDPC_CUDA_TRY(cudaEventCreateWithFlags(&d->stage_free[k], cudaEventDisableTiming));
     }
-    LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->est_pin, sizeof(uint32_t) * RWn * MB, cudaHostAllocDefault));
-    LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->syn_pin, sizeof(uint32_t) * RWm * MB, cudaHostAllocDefault));
-    LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->succ_pin, MB, cudaHostAllocDefault));
-    LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->its_pin, sizeof(int32_t) * MB, cudaHostAllocDefault));
+    if (!d->est_pin) LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->est_pin, sizeof(uint32_t) * RWn * MB, cudaHostAllocDefault));
+    if (!d->syn_pin) LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->syn_pin, sizeof(uint32_t) * RWm * MB, cudaHostAllocDefault));
+    if (!d->succ_pin) LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->succ_pin, MB, cudaHostAllocDefault));
+    if (!d->its_pin) LDPC_CUDA_TRY(cudaHostAlloc((void **)&d->its_pin, sizeof(int32_t) * MB, cudaHostAllocDefault));
+    if (!d->pool.th.empty()) return LDPC_OK;
     // copy threads: every CPU this process may run on (the rank's NUMA-local set when bound), capped
     // at 16; LDPC_COPY_THREADS overrides
     cpu_set_t cs;

@@ -88,3 +88,26 @@ def test_compaction_points_do_not_change_results(cuda, tmp_path, code, B, ebno, 
     for v in ("75", "100"):
         for k in base.files:
             assert np.array_equal(runs[v][k], base[k]), (v, k)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_compaction_random_codes_vs_oracle(cuda, seed):
+    # random irregular codes (some high degrees), batches that do not fill their last chunk, early
+    # stop at an SNR where frames stop at many different rounds: bit-exact vs the oracle
+    from oracle import OracleTables
+
+    from paper_1609_01567_b200 import generate_irregular_code
+
+    rng = np.random.default_rng(100 + seed)
+    m = int(rng.integers(300, 900))
+    prof = {int(rng.integers(4, 9)): int(rng.integers(20, 80)), 3: int(rng.integers(200, 600)), 2: m}
+    extra = {int(rng.integers(17, 70)): 2} if seed % 2 else None
+    H = generate_irregular_code(prof, m, seed=seed, check_degrees=extra)
+    B = int(rng.integers(65, 330))
+    s2 = configs.ebno_to_sigma2(1.0 + 0.5 * seed, configs.rate(H))
+    P = priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((B, H.n)), s2)
+    with ParallelDecoder(CodeTables.from_matrix(H), max_batch=B) as dec:
+        res = dec.decode_priors(P, 25, schedule="stream")
+    est, ok, its, z = OracleTables.from_matrix(H).decode_batch(P, 25)
+    assert np.array_equal(res.iterations, its) and np.array_equal(res.success.astype(bool), ok)
+    assert np.array_equal(res.estimates(), est) and np.array_equal(res.syndromes(), z)
