@@ -3,8 +3,8 @@
 // The same algorithm as the exact kernels -- probability-domain messages, the
 // reference's left-to-right product order (serial.py:63-133), prefix sharing,
 // the den == 0 -> 1/2 and tie -> 1 rules -- evaluated in IEEE fp32 (round to
-// nearest, no FMA contraction, IEEE division).  Messages take 4 bytes, so the
-// HBM roofline doubles.  Results are NOT bit-identical to the fp64 reference:
+// nearest, no FMA contraction; the division is the 2-ulp approximate one for normal
+// denominators).  Messages take 4 bytes, so the HBM roofline doubles.  Results are NOT bit-identical to the fp64 reference:
 // the tolerance (message LLR error and hard-decision agreement) is measured in
 // tests/test_fast_gpu.py and stated in DESIGN.md.
 //
@@ -21,6 +21,13 @@ namespace {
 __device__ __forceinline__ float2 ld2(const float *p) { return __ldcs(reinterpret_cast<const float2 *>(p)); }
 __device__ __forceinline__ void st2(float *p, float x, float y) {
     __stcs(reinterpret_cast<float2 *>(p), make_float2(x, y));
+}
+
+// q = q1 / den in the fast mode: the approximate division (2 ulp) for normal denominators; the
+// IEEE division (with its slow path) only for subnormal ones; den == 0 -> 1/2 (serial.py:86-88)
+__device__ __forceinline__ float fdiv_msg(float q1, float den) {
+    if (den >= 1.17549435e-38f) return __fdividef(q1, den);
+    return den == 0.0f ? 0.5f : __fdiv_rn(q1, den);
 }
 
 template <int D, bool FROM_PRIOR>
@@ -112,8 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_var_f32(NodeLaunch a, float *msg, 
                     q0 = __fmul_rn(q0, om[i][v]);
                     q1 = __fmul_rn(q1, r[i][v]);
                 }
-                const float den = __fadd_rn(q0, q1);
-                out[v] = (den == 0.0f) ? 0.5f : __fdiv_rn(q1, den);
+                out[v] = fdiv_msg(q1, __fadd_rn(q0, q1));
             }
             st2(mb + row_off(pos[k]), out[0], out[1]);
         }

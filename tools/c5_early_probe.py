@@ -9,6 +9,7 @@ sys.path.insert(0, ".")
 from paper_1609_01567_b200 import CodeTables, ParallelDecoder, configs, priors_awgn_batch  # noqa: E402
 
 H = configs.code("C5")
+prec = sys.argv[1] if len(sys.argv) > 1 else "fp64"
 B = 1024
 with ParallelDecoder(CodeTables.from_matrix(H), max_batch=B) as d:
     ws, o = d.workspace(B), d.alloc_outputs(B, torch.device("cuda"))
@@ -17,9 +18,9 @@ with ParallelDecoder(CodeTables.from_matrix(H), max_batch=B) as d:
         P = torch.from_numpy(priors_awgn_batch(-1.0 + np.sqrt(s2) * np.random.default_rng(5).standard_normal((B, H.n)),
                                                s2)).cuda()
         res = {}
-        for label, fn in (("device", lambda: d.decode_device(P, 10, workspace=ws, outputs=o)),
-                          ("channel", lambda: d.decode_channel(7, 0, 0, B, s2, 10, workspace=ws, outputs=o)),
-                          ("fixed", lambda: d.decode_device(P, 10, early_stop=False, workspace=ws, outputs=o))):
+        for label, fn in (("device", lambda: d.decode_device(P, 10, workspace=ws, outputs=o, precision=prec)),
+                          ("channel", lambda: d.decode_channel(7, 0, 0, B, s2, 10, workspace=ws, outputs=o, precision=prec)),
+                          ("fixed", lambda: d.decode_device(P, 10, early_stop=False, workspace=ws, outputs=o, precision=prec))):
             for _ in range(3):
                 fn()
             torch.cuda.synchronize()
