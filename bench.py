@@ -540,7 +540,11 @@ def run_ours(args):
         same = (outs32[0] == outs[0]).all(dim=1).float().mean().item()
         fast = {"value": world * B * H.n / (fms / 1e3) / 1e9, "unit": UNIT, "dtype": "f32", "ms_per_step": fms,
                 "identical_frames_vs_f64": same,
-                "note": "f4 fast mode: same algorithm in fp32 (not bit-exact; tolerance in DESIGN.md)"}
+                "note": "f4 fast mode, fp32: the reference's product order for degrees <= 16 (approximate division), "
+                        "O(d) prefix/suffix checks and log-ratio-sum variables above; not bit-exact, tolerance vs the "
+                        "oracle in DESIGN.md / tests/test_fast_gpu.py",
+                "roofline_frac": (B * survey_bytes_per_codeword(H.total_edges, H.n, iters, w=4) / (fms / 1e3) / 1e9)
+                                 / peak}
 
     # the other BASELINE.json configs (parity-test cases, reported for reference, not the headline):
     # device-timed decode per call through decode_device with the automatic schedule
