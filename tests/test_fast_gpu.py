@@ -146,3 +146,31 @@ def test_all_degrees_through_od_kernels():
                           str(ROOT / "tests" / "test_fast_gpu.py")], capture_output=True, text=True, env=env,
                          cwd=str(ROOT), timeout=900)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_high_degree_codes_vs_oracle(cuda, seed):
+    # random irregular codes with a few checks / variables past one O(d) block pass (> 512 rows) next
+    # to low-degree nodes: message tolerance vs the oracle on random states
+    from oracle import OracleTables
+
+    from paper_1609_01567_b200 import generate_irregular_code
+
+    rng = np.random.default_rng(500 + seed)
+    m = 1400
+    H = generate_irregular_code({600 + 50 * seed: 1, 40: 4, 3: 900, 2: 1000}, m, seed=seed,
+                                check_degrees={700 + 100 * seed: 1, 130: 2})
+    T, O = CodeTables.from_matrix(H), OracleTables.from_matrix(H)
+    P = rng.uniform(0.2, 0.8, size=(2, H.n))
+    R = rng.uniform(0.45, 0.55, size=(2, H.total_edges))
+    Q = rng.uniform(0.45, 0.55, size=(2, H.total_edges))
+    c_fast = values_to_variable(Q, T, precision="fp32")
+    v_fast = values_to_check(P, R, T, precision="fp32")
+    for b in range(2):
+        c_ref = O.values_to_variable(Q[b])
+        ok = _unsaturated(c_ref)
+        assert np.abs(_llr(c_fast[b][ok]) - _llr(c_ref[ok])).max() <= C_PHASE_TOL
+        v_ref = O.values_to_check(P[b], R[b])
+        ok = _unsaturated(v_ref)
+        d = np.abs(_llr(v_fast[b][ok]) - _llr(v_ref[ok]))
+        assert d.mean() <= V_PHASE_MEAN and d.max() <= V_PHASE_MAX, (d.mean(), d.max())
