@@ -111,3 +111,37 @@ def test_compaction_random_codes_vs_oracle(cuda, seed):
     est, ok, its, z = OracleTables.from_matrix(H).decode_batch(P, 25)
     assert np.array_equal(res.iterations, its) and np.array_equal(res.success.astype(bool), ok)
     assert np.array_equal(res.estimates(), est) and np.array_equal(res.syndromes(), z)
+
+
+def test_concurrent_decoders_and_shared_decoder(cuda):
+    # host threads: two decoders at once (each its own streams, fork sets and compaction side
+    # streams) and two threads sharing one decoder (serialised by its lock); early stop with
+    # compaction and forked high-degree buckets (C4) -- every result equals the oracle
+    import threading
+
+    from oracle import OracleTables
+
+    H = configs.code("C4")
+    T = CodeTables.from_matrix(H)
+    frames = [_frames("C4", 96, 3.0, seed=s)[1] for s in range(4)]
+    O = OracleTables.from_matrix(H)
+    want = [O.decode_batch(P, 12) for P in frames]
+    got, errors = [None] * 4, []
+
+    def run(dec, i):
+        try:
+            got[i] = dec.decode_priors(frames[i], 12, schedule="stream")
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    with ParallelDecoder(T, max_batch=96) as d0, ParallelDecoder(T, max_batch=96) as d1:
+        ts = [threading.Thread(target=run, args=(d0, 0)), threading.Thread(target=run, args=(d1, 1)),
+              threading.Thread(target=run, args=(d0, 2)), threading.Thread(target=run, args=(d1, 3))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    assert not errors, errors
+    for res, (est, ok, its, z) in zip(got, want):
+        assert np.array_equal(res.iterations, its) and np.array_equal(res.estimates(), est)
+        assert np.array_equal(res.success.astype(bool), ok) and np.array_equal(res.syndromes(), z)
