@@ -623,7 +623,9 @@ extern "C" size_t ldpc_workspace_bytes(const ldpc_graph *g, int32_t B) {
 
 // grid schedule by default for B <= kGridMaxB while its working set stays well inside the L2
 // (LDPC_GRID=0 disables the automatic choice)
-constexpr size_t kGridAutoBytes = 40ull << 20;  // measured crossover: C3 B = 16 grid 2.97 ms vs stream 4.14, B = 32 5.08 vs 4.13
+// grid vs stream, device time per decode (tools/grid_vs_stream.py, 2 dB, early stop, 50 rounds):
+// C3 B = 16 1.45 vs 4.15 ms, B = 32 2.67 vs 4.16 ms (75 MB working set); C2 B = 32 0.35 vs 1.46 ms
+constexpr size_t kGridAutoBytes = 96ull << 20;
 static bool grid_auto() {
     static const bool on = [] {
         const char *e = getenv("LDPC_GRID");

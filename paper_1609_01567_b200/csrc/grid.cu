@@ -4,9 +4,10 @@
 // per iteration move the padded chunk through HBM: a single C3 frame costs what 64 do
 // (2.9 ms at 16 iterations).  For B <= kGridMaxB codewords of a code too large for the
 // on-chip schedule, one cooperative grid (every SM, all blocks resident) instead keeps
-// the B codewords' messages in a codeword-major workspace (B * E * 8 bytes: 1.8 MB per C3
+// the B codewords' messages in a workspace (B * E * 8 bytes: 1.8 MB per C3
 // codeword, L2-resident) and runs Algorithm 2 with grid-wide barriers, one thread per
-// (node, codeword) item:
+// (node, codeword) item (codeword-minor layout, node-major items: a warp's accesses to a message
+// row are one contiguous run):
 //   init:   priors (or observations -> priors, priors.cuh), zeroed outputs and flags
 //   pre:    C-phase from the priors (serial.py:166)
 //   round t (serial.py:165-178), two barriers, as the on-chip kernel:
@@ -47,11 +48,15 @@ struct GridArgs {
     int64_t E;
 };
 
+// Layout: codeword-minor -- msg[E][B], pr[n][B], chat[n][B] -- and items ordered node-major
+// (item k = node k / B, codeword k % B), so the 32 lanes of a warp are consecutive codewords of one
+// node (or a few nodes when B < 32) and each message row a warp touches is one contiguous run.
 struct GridAcc {  // nodes.cuh accessor for codeword cw
-    double *msg;
-    const double *pr;
-    __device__ __forceinline__ double *slot(int s) const { return msg + s; }
-    __device__ __forceinline__ double prior_of(int v) const { return pr[v]; }
+    double *msg;        // &msg[0][cw]
+    const double *pr;   // &pr[0][cw]
+    int32_t B;
+    __device__ __forceinline__ double *slot(int s) const { return msg + (size_t)s * B; }
+    __device__ __forceinline__ double prior_of(int v) const { return pr[(size_t)v * B]; }
 };
 
 __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ GridArgs a) {
@@ -60,12 +65,13 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     const int64_t nB = (int64_t)a.n * a.B, mB = (int64_t)a.m * a.B;
     const uint32_t all = (a.B >= 32) ? 0xffffffffu : ((1u << a.B) - 1u);
-    auto acc = [&](int cw) { return GridAcc{a.msg + (size_t)cw * a.E, a.pr + (size_t)cw * a.n}; };
+    auto acc = [&](int cw) { return GridAcc{a.msg + cw, a.pr + cw, a.B}; };
 
-    // init
+    // init: [B][n] input -> pr[n][B]
     for (int64_t k = tid; k < nB; k += T) {
-        const double x = __ldg(a.in + k);
-        a.pr[k] = a.sig2 ? awgn_prior(x, __ldg(a.sig2 + k / a.n)) : x;
+        const int v = (int)(k / a.B), cw = (int)(k - (int64_t)v * a.B);
+        const double x = __ldg(a.in + (size_t)cw * a.n + v);
+        a.pr[k] = a.sig2 ? awgn_prior(x, __ldg(a.sig2 + cw)) : x;
     }
     for (int64_t k = tid; k < (int64_t)a.B * a.RWn; k += T) a.est[k] = 0u;
     if (a.syn)
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
     grid.sync();
     // pre-pass C-phase from the priors
     for (int64_t k = tid; k < mB; k += T) {
-        const int cw = (int)(k / a.m), c = (int)(k - (int64_t)cw * a.m);
+        const int c = (int)(k / a.B), cw = (int)(k - (int64_t)c * a.B);
         check_node<true>(acc(cw), a.tb, c);
     }
     grid.sync();
@@ -84,9 +90,8 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
         const bool more = t < a.max_iter;
         // VE
         for (int64_t k = tid; k < nB; k += T) {
-            const int cw = (int)(k / a.n);
+            const int v = (int)(k / a.B), cw = (int)(k - (int64_t)v * a.B);
             if ((done >> cw) & 1u) continue;
-            const int v = (int)(k - (int64_t)cw * a.n);
             a.chat[k] = var_node(acc(cw), a.tb, v, more, a.pr[k]);
         }
         grid.sync();
@@ -94,13 +99,12 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
         if (tid == 0) a.unsat[(t + 1) & 1] = 0u;
         uint32_t unsat = 0;
         for (int64_t k = tid; k < mB; k += T) {
-            const int cw = (int)(k / a.m);
+            const int c = (int)(k / a.B), cw = (int)(k - (int64_t)c * a.B);
             if ((done >> cw) & 1u) continue;
-            const int c = (int)(k - (int64_t)cw * a.m);
             const int s0 = __ldg(a.tb.chk_off + c), d = __ldg(a.tb.chk_off + c + 1) - s0;
-            const uint8_t *ch = a.chat + (size_t)cw * a.n;
+            const uint8_t *ch = a.chat + cw;
             int z = 0;
-            for (int i = 0; i < d; i++) z ^= ch[__ldg(a.tb.chk_var + s0 + i)];
+            for (int i = 0; i < d; i++) z ^= ch[(size_t)__ldg(a.tb.chk_var + s0 + i) * a.B];
             if (z) unsat |= 1u << cw;
             if (more) check_node<false>(acc(cw), a.tb, c);
         }
@@ -126,16 +130,16 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
     // packed estimate and syndrome rows of the final state
     for (int64_t k = tid; k < nB; k += T) {
         if (!a.chat[k]) continue;
-        const int cw = (int)(k / a.n), v = (int)(k - (int64_t)cw * a.n);
+        const int v = (int)(k / a.B), cw = (int)(k - (int64_t)v * a.B);
         atomicOr(a.est + (size_t)cw * a.RWn + (v >> 5), 1u << (v & 31));
     }
     if (a.syn)
         for (int64_t k = tid; k < mB; k += T) {
-            const int cw = (int)(k / a.m), c = (int)(k - (int64_t)cw * a.m);
+            const int c = (int)(k / a.B), cw = (int)(k - (int64_t)c * a.B);
             const int s0 = __ldg(a.tb.chk_off + c), d = __ldg(a.tb.chk_off + c + 1) - s0;
-            const uint8_t *ch = a.chat + (size_t)cw * a.n;
+            const uint8_t *ch = a.chat + cw;
             int z = 0;
-            for (int i = 0; i < d; i++) z ^= ch[__ldg(a.tb.chk_var + s0 + i)];
+            for (int i = 0; i < d; i++) z ^= ch[(size_t)__ldg(a.tb.chk_var + s0 + i) * a.B];
             if (z) atomicOr(a.syn + (size_t)cw * a.RWm + (c >> 5), 1u << (c & 31));
         }
 }
