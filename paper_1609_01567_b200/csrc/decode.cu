@@ -539,15 +539,25 @@ static int decode_view(const ldpc_graph *g, const Workspace &w, int32_t max_iter
             // the priors move and the stopped codewords retire beside the check phase (joined before
             // the next variable phase, which reads both); eager profiling keeps one stream
             cf = prof.out == nullptr ? compact_fork(s) : nullptr;
-            RUN(LDPC_KCLASS_LAYOUT, 0, launch_compact(g, w, t - 1, compact_pct(), *out, fast ? f32 : exact, fast ? 3 : 2, s,
-                                                      cf ? cf->side : nullptr, cf ? cf->fork : nullptr));
+            if (cf == nullptr) {
+                RUN(LDPC_KCLASS_LAYOUT, 0, launch_compact(g, w, t - 1, compact_pct(), *out, fast ? f32 : exact,
+                                                          fast ? 3 : 2, s));
+            } else {
+                // (no profiling here: prof is inactive whenever the side stream is used)
+                int rc = launch_compact(g, w, t - 1, compact_pct(), *out, fast ? f32 : exact, fast ? 3 : 2, s,
+                                        cf->side, cf->fork);
+                if (rc == LDPC_OK) rc = check_phase(g, w, false, done, s, fast);
+                // join even after an error, so no stream is left forked (a capture could not end)
+                const cudaError_t e1 = cudaEventRecord(cf->join, cf->side);
+                const cudaError_t e2 = cudaStreamWaitEvent(s, cf->join, 0);
+                cf = nullptr;
+                if (rc) return rc;
+                LDPC_CUDA_TRY(e1);
+                LDPC_CUDA_TRY(e2);
+                continue;
+            }
         }
         RUN(LDPC_KCLASS_CHECK, c_bytes, check_phase(g, w, false, done, s, fast));
-        if (cf != nullptr) {
-            LDPC_CUDA_TRY(cudaEventRecord(cf->join, cf->side));
-            LDPC_CUDA_TRY(cudaStreamWaitEvent(s, cf->join, 0));
-            cf = nullptr;
-        }
     }
     RUN(LDPC_KCLASS_ESTIMATE, e_bytes, var_phase(g, w, false, done, s, fast));
     RUN(LDPC_KCLASS_SYNDROME, s_bytes + (m / 8) * B, launch_syndrome(g, w, true, early, s));
