@@ -247,9 +247,9 @@ static thread_local int g_sweep = 0;  // direction of the next node-kernel launc
 // A phase is one launch per degree bucket (plus one for the high-degree range).  Memory-bound
 // launches of the big buckets stay in order on the calling stream (run side by side they only
 // split the bandwidth: profiles/r1_kernel_choice.md); launches of buckets holding less than
-// 1/kSmallShare of the edges -- latency-bound, a few blocks per SM, mostly the compute-bound
-// high-degree ones -- go to side streams forked from and joined back into the calling stream, so
-// they overlap each other and the big ones.  Buckets write disjoint slots and c_hat rows, so the
+// 1/kSmallShare of the edges (latency-bound, a few blocks per SM) and every launch of the mid- and
+// high-degree kernels (compute-bound: O(d^2) ordered fp64 products) go to side streams forked from
+// and joined back into the calling stream, so they overlap each other and the big ones.  Buckets write disjoint slots and c_hat rows, so the
 // order is free.  Also inside CUDA-graph capture (the side streams join the capture through the
 // fork event).  LDPC_FORK=0 keeps every launch on the calling stream.
 constexpr int kSideStreams = 3;
@@ -355,7 +355,6 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
         return run_phase(L, s);
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
-    int64_t wide_edges = 0;
     for (const Bucket &b : g->chk_buckets) {
         if (b.deg <= kMaxMidCheckDegree) {
             NodeLaunch a = a0;
@@ -369,20 +368,18 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
                                     : use_ring(false, deg)    ? launch_check_pipe(a, deg, from_prior, st)
                                                               : launch_check_bucket(a, deg, from_prior, st);
                          },
-                         small((int64_t)b.node_count * b.deg)});
+                         small((int64_t)b.node_count * b.deg) || deg > kMaxRegCheckDegree});
         } else {
             if (wide_begin < 0) wide_begin = b.node_begin;
             wide_end = b.node_begin + b.node_count;
             wide_max = std::max(wide_max, b.deg);
-            wide_edges += (int64_t)b.node_count * b.deg;
         }
     }
-    if (wide_begin >= 0) {
+    if (wide_begin >= 0) {  // compute-bound (O(d^2) fp64): beside the memory-bound buckets
         NodeLaunch a = a0;
         a.node_begin = wide_begin;
         a.node_count = wide_end - wide_begin;
-        L.push_back({[=](cudaStream_t st) { return launch_check_wide(a, wide_max, from_prior, st); },
-                     small(wide_edges)});
+        L.push_back({[=](cudaStream_t st) { return launch_check_wide(a, wide_max, from_prior, st); }, true});
     }
     return run_phase(L, s);
 }
@@ -414,7 +411,6 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
         return run_phase(L, s);
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
-    int64_t wide_edges = 0;
     for (const Bucket &b : g->var_buckets) {
         if (b.deg <= kMaxMidVarDegree) {
             NodeLaunch a = a0;
@@ -428,19 +424,18 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
                                     : use_ring(true, deg) ? launch_var_pipe(a, deg, write_q, st)
                                                           : launch_var_bucket(a, deg, write_q, st);
                          },
-                         small((int64_t)b.node_count * b.deg)});
+                         small((int64_t)b.node_count * b.deg) || deg > kMaxRegDegree});
         } else {
             if (wide_begin < 0) wide_begin = b.node_begin;
             wide_end = b.node_begin + b.node_count;
             wide_max = std::max(wide_max, b.deg);
-            wide_edges += (int64_t)b.node_count * b.deg;
         }
     }
-    if (wide_begin >= 0) {
+    if (wide_begin >= 0) {  // compute-bound (O(d^2) fp64): beside the memory-bound buckets
         NodeLaunch a = a0;
         a.node_begin = wide_begin;
         a.node_count = wide_end - wide_begin;
-        L.push_back({[=](cudaStream_t st) { return launch_var_wide(a, wide_max, write_q, st); }, small(wide_edges)});
+        L.push_back({[=](cudaStream_t st) { return launch_var_wide(a, wide_max, write_q, st); }, true});
     }
     return run_phase(L, s);
 }
