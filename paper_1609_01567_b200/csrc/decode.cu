@@ -351,7 +351,7 @@ int check_phase(const ldpc_graph *g, const Workspace &w, bool from_prior, const 
                              return launch_fast_od_class(a0, c, false, from_prior, msg32(g, w), prior32(g, w),
                                                          w.od_scratch, w.od_stride, kOdScratchBlocks, st);
                          },
-                         small(c.edges)});
+                         true});  // O(d) classes: few blocks per SM, latency-bound
         return run_phase(L, s);
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
@@ -407,7 +407,7 @@ int var_phase(const ldpc_graph *g, const Workspace &w, bool write_q, const uint3
                              return launch_fast_od_class(a0, c, true, write_q, msg32(g, w), nullptr, nullptr, 0, 0,
                                                          st);
                          },
-                         small(c.edges)});
+                         true});  // O(d) classes: few blocks per SM, latency-bound
         return run_phase(L, s);
     }
     int wide_begin = -1, wide_end = 0, wide_max = 0;
