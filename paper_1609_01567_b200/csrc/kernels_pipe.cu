@@ -159,6 +159,18 @@ __device__ __forceinline__ bool all_done(const DoneMask &m) {
 //   lanes 0..D-1: message slots of the node's edges (outputs; inputs unless FROM_PRIOR)
 //   variables: lane D = the variable (its prior row and c_hat row)
 //   checks FROM_PRIOR: lanes 16..16+D-1 = variables whose prior rows are the inputs
+// NPT nodes per task (low-degree variables): lanes u*(D+1) .. u*(D+1)+D hold node u's D slots and
+// its variable; a missing last node gets variable -1 (skipped) and slot 0 (a harmless fetch)
+template <int D, int NPT>
+__device__ __forceinline__ int load_id_npt(const NodeLaunch &a, int ni, int lane) {
+    const int u = lane / (D + 1), j = lane - u * (D + 1);
+    const int node = ni * NPT + u;
+    if (u >= NPT) return 0;
+    if (node >= a.node_count) return j == D ? -1 : 0;
+    if (j < D) return __ldg(a.slot_ord + a.edge_begin + node * D + j);
+    return __ldg(a.order + a.node_begin + node);
+}
+
 template <int D, bool IS_VAR, bool FROM_PRIOR>
 __device__ __forceinline__ int load_id(const NodeLaunch &a, int ni, int lane) {
     const int32_t base = a.edge_begin + ni * D;
@@ -179,6 +191,41 @@ template <int D, bool IS_VAR>
 constexpr bool prior_in_ring() { return IS_VAR && D < kPriorRegDeg; }
 template <int D, bool IS_VAR>
 constexpr int ring_rows() { return D + (prior_in_ring<D, IS_VAR>() ? 1 : 0); }
+
+template <int D, int V, bool EARLY, int NPT>
+__device__ __forceinline__ void issue_npt(const NodeLaunch &a, double *rows, int *ids_s, int ch, int id,
+                                          const DoneMask &dm, int lane) {
+    static_assert(prior_in_ring<D, true>(), "NPT > 1 needs the prior row in the ring");
+    constexpr int ROWS = ring_rows<D, true>();  // per node: D message rows + the prior row
+    constexpr int ROW = 32 * V;
+    constexpr int RPI = V == 2 ? 1 : 2;
+    const bool skip = EARLY && all_done<V>(dm);
+    ids_s[lane] = id;
+    if (lane == 0) {
+        ids_s[32] = ch;
+        if constexpr (EARLY) {
+            ids_s[33] = skip ? 1 : 0;
+            ids_s[34] = (int)dm.w0;
+            ids_s[35] = (int)dm.w1;
+        }
+    }
+    if (skip) return;
+    const int cw0 = ch * 32 * V;
+    const int sub = V == 2 ? 0 : (lane >> 4);
+    const int piece = V == 2 ? lane : (lane & 15);
+    const double *mb = chunk_base(a.msg, a.msg_rows, cw0) + 2 * piece;
+    const double *pb = chunk_base(a.P, a.p_rows, cw0) + 2 * piece;
+    double *dst = rows + 2 * piece;
+#pragma unroll
+    for (int j = 0; j < (NPT * ROWS + RPI - 1) / RPI; j++) {
+        const int r = j * RPI + sub;
+        const int rr = r < NPT * ROWS ? r : NPT * ROWS - 1;
+        const int u = rr / ROWS, k = rr - u * ROWS;  // node u of the task, its row k (k == D: prior)
+        const int src_id = max(0, __shfl_sync(0xffffffffu, id, u * (D + 1) + k));
+        const double *src = (k == D ? pb : mb) + row_off(src_id);
+        if (r < NPT * ROWS) cp_async16(dst + r * ROW, src);
+    }
+}
 
 template <int D, int V, bool IS_VAR, bool FROM_PRIOR, bool EARLY>
 __device__ __forceinline__ void issue(const NodeLaunch &a, double *rows, int *ids_s, int ch, int id,
@@ -293,7 +340,7 @@ __device__ __forceinline__ void compute_check(const NodeLaunch &a, const double 
 
 template <int D, int V, bool WRITE_Q, bool EARLY>
 __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *rows, const int *ids, int ch,
-                                            int lane, const double (&pj)[V]) {
+                                            int lane, const double (&pj)[V], const int *masks) {
     constexpr int ROW = 32 * V;
     double *mb = chunk_base(a.msg, a.msg_rows, ch * 32 * V) + lane * V;
     double r[D][V], om[D][V];
@@ -370,7 +417,7 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
             uint32_t hi = part1by1(even >> 16) | (part1by1(odd >> 16) << 1);
             uint32_t *dst = row + 2 * ch;
             if constexpr (EARLY) {
-                const uint32_t d0 = (uint32_t)ids[34], d1 = (uint32_t)ids[35];  // prefetched done mask
+                const uint32_t d0 = (uint32_t)masks[0], d1 = (uint32_t)masks[1];  // prefetched done mask
                 if (d0) lo = (lo & ~d0) | (dst[0] & d0);
                 if (d1) hi = (hi & ~d1) | (dst[1] & d1);
             }
@@ -380,7 +427,7 @@ __device__ __forceinline__ void compute_var(const NodeLaunch &a, const double *r
         uint32_t bits = __ballot_sync(0xffffffffu, !(p0[0] > p1[0]));
         if (lane == 0) {
             if constexpr (EARLY) {
-                const uint32_t d0 = (uint32_t)ids[34];  // prefetched done mask
+                const uint32_t d0 = (uint32_t)masks[0];  // prefetched done mask
                 if (d0) bits = (bits & ~d0) | (row[ch] & d0);
             }
             row[ch] = bits;
@@ -402,14 +449,16 @@ __device__ __forceinline__ void load_prior(const NodeLaunch &a, int node, int ch
 }
 
 // EARLY: early-stop mode (a.done != nullptr): per-task chunk-done masks, read ahead with the ids
-template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY, bool TMA = false>  // FLAG: FROM_PRIOR / WRITE_Q
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY, bool TMA = false, int NPT = 1>  // FLAG: FROM_PRIOR / WRITE_Q
 __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, int64_t first, int64_t W,
                                           unsigned char *wsm, const TMap *tm_msg = nullptr,
                                           const TMap *tm_p = nullptr) {
     // one warp's persistent task loop: tasks first, first + W, ... of a side's bucket,
-    // its ring (ids + stages) at wsm
+    // its ring (ids + stages) at wsm; a task is NPT nodes (NPT > 1: low-degree variables)
     static_assert(!TMA || IS_VAR, "the TMA ring serves the variable side");
-    constexpr int ROWS = ring_rows<D, IS_VAR>();
+    static_assert(NPT == 1 || (IS_VAR && !TMA && NPT * (D + 1) <= 32), "NPT > 1: variables, ids in one warp");
+    constexpr int ROWS = NPT * ring_rows<D, IS_VAR>();  // rows per stage
+    constexpr int NROWS = ring_rows<D, IS_VAR>();       // rows per node
     constexpr bool PREG = IS_VAR && !prior_in_ring<D, IS_VAR>();  // prior via registers
     constexpr int ROW = 32 * V;
     constexpr bool FP = !IS_VAR && FLAG;
@@ -428,23 +477,28 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
     }
     // early-stop compaction: only the active chunks' tasks (chunk-major, so a prefix of the tasks)
     const int wchunks = active_chunks(a, a.Bp / (32 * V), 32 * V);
-    ntasks = min(ntasks, (int64_t)a.node_count * wchunks);
+    const int ncs = (a.node_count + NPT - 1) / NPT;  // tasks per chunk
+    ntasks = min(ntasks, (int64_t)ncs * wchunks);
     if (first >= ntasks) return;
     const int ntask = (int)((ntasks - first + W - 1) / W);  // this warp's tasks: first, first + W, ...
+    auto load_ids = [&](int ni) {
+        if constexpr (NPT > 1) return load_id_npt<D, NPT>(a, ni, lane);
+        else return load_id<D, IS_VAR, FP>(a, ni, lane);
+    };
 
     // The row ids of task j are loaded two issues ahead (while task j - 2 is
     // issued), so the index loads' L2 latency is off the critical path; the
     // cursor runs two tasks ahead of the issue.
-    TaskCursor cur(first, W, a.node_count);
+    TaskCursor cur(first, W, ncs);
     const int chunks_m1 = wchunks - 1;  // reverse sweep: chunk c -> chunks-1-c
     auto chunk_of = [&](int c) { return a.reverse ? chunks_m1 - c : c; };
-    int nid0 = load_id<D, IS_VAR, FP>(a, cur.ni, lane), nch0 = chunk_of(cur.ch);
+    int nid0 = load_ids(cur.ni), nch0 = chunk_of(cur.ch);
     DoneMask nd0 = EARLY ? load_done<V>(a.done, nch0) : DoneMask{};
     cur.next();
     int nid1 = 0, nch1 = 0;
     DoneMask nd1;
     if (ntask > 1) {
-        nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
+        nid1 = load_ids(cur.ni);
         nch1 = chunk_of(cur.ch);
         if (EARLY) nd1 = load_done<V>(a.done, nch1);
         cur.next();
@@ -456,7 +510,7 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
         nch0 = nch1;
         nd0 = nd1;
         if (j + 2 < ntask) {
-            nid1 = load_id<D, IS_VAR, FP>(a, cur.ni, lane);
+            nid1 = load_ids(cur.ni);
             nch1 = chunk_of(cur.ch);
             if (EARLY) nd1 = load_done<V>(a.done, nch1);
             cur.next();
@@ -465,6 +519,8 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
         if constexpr (TMA)
             issue_tma<D, V, EARLY>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, bars + sj, ich, id, idone,
                                    lane, tm_msg, tm_p);
+        else if constexpr (NPT > 1)
+            issue_npt<D, V, EARLY, NPT>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, idone, lane);
         else
             issue<D, V, IS_VAR, FP, EARLY>(a, rows + (size_t)sj * ROWS * ROW, ids + sj * kIdsStride, ich, id, idone,
                                            lane);
@@ -512,25 +568,37 @@ __device__ __forceinline__ void ring_loop(const NodeLaunch &a, int64_t ntasks, i
                 const int *idsn = ids + ((it + PD) % S) * kIdsStride;
                 load_prior<V>(a, idsn[D], idsn[32], lane, pq[PD - 1]);
             }
-        } else if constexpr (IS_VAR) {
+        } else if constexpr (IS_VAR && NPT == 1) {
             ld_smem<V>(rows + (size_t)s * ROWS * ROW + D * ROW + V * lane, pj);
         }
         if (EARLY ? !ids_s[33] : !wchunk_done<V>(a.done, ch)) {
-            if constexpr (IS_VAR) compute_var<D, V, FLAG, EARLY>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane, pj);
-            else compute_check<D, V>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane);
+            if constexpr (NPT > 1) {
+#pragma unroll
+                for (int u = 0; u < NPT; u++) {
+                    if (ids_s[u * (D + 1) + D] < 0) break;  // a missing last node (warp-uniform)
+                    const double *nrows = rows + (size_t)s * ROWS * ROW + (size_t)u * NROWS * ROW;
+                    ld_smem<V>(nrows + D * ROW + V * lane, pj);
+                    compute_var<D, V, FLAG, EARLY>(a, nrows, ids_s + u * (D + 1), ch, lane, pj, ids_s + 34);
+                }
+            } else if constexpr (IS_VAR) {
+                compute_var<D, V, FLAG, EARLY>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane, pj, ids_s + 34);
+            } else {
+                compute_check<D, V>(a, rows + (size_t)s * ROWS * ROW, ids_s, ch, lane);
+            }
         }
         __syncwarp();  // stage s is reused by the issue of the next iteration
     }
     if constexpr (!TMA) cp_wait<0>();
 }
 
-template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY>  // FLAG: FROM_PRIOR / WRITE_Q
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY, int NPT = 1>  // FLAG: FROM_PRIOR / WRITE_Q
 __global__ void __launch_bounds__(kThreads, MINB) k_node_ring(NodeLaunch a, int64_t ntasks) {
-    using R = Ring<ring_rows<D, IS_VAR>(), V, MINB>;
+    using R = Ring<NPT * ring_rows<D, IS_VAR>(), V, MINB>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5;
-    ring_loop<D, V, IS_VAR, FLAG, MINB, EARLY>(a, ntasks, (int64_t)blockIdx.x * kWarpsPerBlock + warp,
-                                        (int64_t)gridDim.x * kWarpsPerBlock, smem + (size_t)warp * R::kBytes);
+    ring_loop<D, V, IS_VAR, FLAG, MINB, EARLY, false, NPT>(a, ntasks, (int64_t)blockIdx.x * kWarpsPerBlock + warp,
+                                                          (int64_t)gridDim.x * kWarpsPerBlock,
+                                                          smem + (size_t)warp * R::kBytes);
 }
 
 template <int D, int V, bool WRITE_Q, int MINB, bool EARLY>
@@ -556,11 +624,11 @@ int ring_v(bool var_side, int deg) {
     return var_side && deg >= 3 ? 1 : 2;
 }
 
-template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY>
+template <int D, int V, bool IS_VAR, bool FLAG, int MINB, bool EARLY, int NPT = 1>
 int launch_ring_ve(const NodeLaunch &a, cudaStream_t st) {
-    constexpr int ROWS = ring_rows<D, IS_VAR>();
+    constexpr int ROWS = NPT * ring_rows<D, IS_VAR>();
     const size_t smem = (size_t)kWarpsPerBlock * Ring<ROWS, V, MINB>::kBytes;
-    auto kern = k_node_ring<D, V, IS_VAR, FLAG, MINB, EARLY>;
+    auto kern = k_node_ring<D, V, IS_VAR, FLAG, MINB, EARLY, NPT>;
     // the shared-memory attribute is per device: set it (and size the grid) once per device
     constexpr int kMaxDevices = 64;
     static int per_sm_of[kMaxDevices] = {}, sms_of[kMaxDevices] = {};
@@ -585,7 +653,7 @@ int launch_ring_ve(const NodeLaunch &a, cudaStream_t st) {
         per_sm = per_sm_of[dev];
         sms = sms_of[dev];
     }
-    const int64_t ntasks = (int64_t)a.node_count * (a.Bp / (32 * V));
+    const int64_t ntasks = (int64_t)((a.node_count + NPT - 1) / NPT) * (a.Bp / (32 * V));
     if (ntasks == 0) return LDPC_OK;
     const int64_t need = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int64_t blocks = std::min<int64_t>(need, (int64_t)per_sm * sms);
@@ -684,12 +752,30 @@ bool use_tma_ring() {
 
 // variables get a fixed-iteration instantiation without the early-stop bookkeeping; checks
 // (ring only on request) keep the one that handles both modes
+// Nodes per ring task for the shortest variable tasks: two for degree 2 and for the final estimate
+// pass (no q writes) of degree 3, halving their per-task overhead; measured per launch (ncu, C3):
+// deg 2 226.3 -> 224.8 us, deg-2 estimate 145.1 -> 134.2, deg-3 estimate 113.6 -> 96.7, but deg 3
+// with q writes 195.9 -> 198.2 (kept at one).  LDPC_RING_NPT=1|2 forces one choice for degrees <= 3.
+int ring_npt(int deg, bool write_q) {
+    static const int forced = [] {
+        const char *e = getenv("LDPC_RING_NPT");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced == 1 || forced == 2) return forced;
+    return (deg == 2 || (deg == 3 && !write_q)) ? 2 : 1;
+}
+
 template <int D, int V, bool IS_VAR, bool FLAG, int MINB>
 int launch_ring_v(const NodeLaunch &a, cudaStream_t st) {
     if constexpr (IS_VAR) {
         if (use_tma_ring() && a.Bp % 64 == 0)
             return a.done == nullptr ? launch_var_tma_ve<D, V, FLAG, MINB, false>(a, st)
                                      : launch_var_tma_ve<D, V, FLAG, MINB, true>(a, st);
+        if constexpr (D <= 3) {
+            if (ring_npt(D, FLAG) == 2)
+                return a.done == nullptr ? launch_ring_ve<D, V, IS_VAR, FLAG, MINB, false, 2>(a, st)
+                                         : launch_ring_ve<D, V, IS_VAR, FLAG, MINB, true, 2>(a, st);
+        }
         if (a.done == nullptr) return launch_ring_ve<D, V, IS_VAR, FLAG, MINB, false>(a, st);
     }
     return launch_ring_ve<D, V, IS_VAR, FLAG, MINB, true>(a, st);
