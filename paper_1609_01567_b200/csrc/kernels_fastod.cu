@@ -254,7 +254,6 @@ int fast_od_scratch_stride(const ldpc_graph *g) {
     return J > 1 ? J * 32 : 0;
 }
 
-// Every bucket of the side with degree >= min_deg, grouped into launches by warps per block.
 // The buckets of degree >= min_deg grouped into launches by warps per block (buckets are sorted by
 // degree, so a class is a contiguous node range).
 std::vector<OdClass> fast_od_classes(const std::vector<Bucket> &buckets, int min_deg) {
