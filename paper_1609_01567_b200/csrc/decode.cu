@@ -84,6 +84,9 @@ size_t workspace_bytes(const ldpc_graph *g, int32_t B) {
     b += align256(sizeof(int32_t) * Bp);
     b += align256(sizeof(float) * (size_t)kOdScratchBlocks * fast_od_scratch_stride(g));
     b += align256(sizeof(int32_t) * Bp) * 3 + align256(sizeof(uint32_t) * NW) + align256(sizeof(int32_t) * 8);
+    // the same workspace serves the grid schedule for small batches (codeword-minor, B bytes per variable
+    // for the hard decisions)
+    if (B <= kGridMaxB) b = std::max(b, grid_workspace_bytes(g, B));
     return b;
 }
 

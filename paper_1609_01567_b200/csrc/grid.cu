@@ -40,7 +40,7 @@ struct GridArgs {
     double *msg;           // [B][E]
     double *pr;            // [B][n]
     uint8_t *chat;         // [B][n]
-    uint32_t *unsat;       // [2]: bit cw = codeword cw unsatisfied, by round parity
+    unsigned long long *unsat;  // [2]: bit cw = codeword cw unsatisfied, by round parity
     uint32_t *est;         // [B][RWn]
     uint8_t *succ;         // [B]
     int32_t *iters;        // [B]
@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     const int64_t nB = (int64_t)a.n * a.B, mB = (int64_t)a.m * a.B;
-    const uint32_t all = (a.B >= 32) ? 0xffffffffu : ((1u << a.B) - 1u);
+    using Mask = unsigned long long;  // one bit per codeword (B <= 64)
+    const Mask all = (a.B >= 64) ? ~0ull : ((1ull << a.B) - 1ull);
     auto acc = [&](int cw) { return GridAcc{a.msg + cw, a.pr + cw, a.B}; };
 
     // init: [B][n] input -> pr[n][B]
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
     for (int64_t k = tid; k < (int64_t)a.B * a.RWn; k += T) a.est[k] = 0u;
     if (a.syn)
         for (int64_t k = tid; k < (int64_t)a.B * a.RWm; k += T) a.syn[k] = 0u;
-    if (tid < 2) a.unsat[tid] = 0u;
+    if (tid < 2) a.unsat[tid] = 0ull;
     grid.sync();
     // pre-pass C-phase from the priors
     for (int64_t k = tid; k < mB; k += T) {
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
         check_node<true>(acc(cw), a.tb, c);
     }
     grid.sync();
-    uint32_t done = 0;  // identical in every thread: derived from the same flags after a barrier
+    Mask done = 0;  // identical in every thread: derived from the same flags after a barrier
     int t = 0;
     for (;; t++) {
         const bool more = t < a.max_iter;
@@ -96,8 +97,8 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
         }
         grid.sync();
         // SC; the other parity's flag was last read before the VE barrier: reset it for round t+1
-        if (tid == 0) a.unsat[(t + 1) & 1] = 0u;
-        uint32_t unsat = 0;
+        if (tid == 0) a.unsat[(t + 1) & 1] = 0ull;
+        Mask unsat = 0;
         for (int64_t k = tid; k < mB; k += T) {
             const int c = (int)(k / a.B), cw = (int)(k - (int64_t)c * a.B);
             if ((done >> cw) & 1u) continue;
@@ -105,15 +106,15 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
             const uint8_t *ch = a.chat + cw;
             int z = 0;
             for (int i = 0; i < d; i++) z ^= ch[(size_t)__ldg(a.tb.chk_var + s0 + i) * a.B];
-            if (z) unsat |= 1u << cw;
+            if (z) unsat |= 1ull << cw;
             if (more) check_node<false>(acc(cw), a.tb, c);
         }
         // one atomic per warp
         for (int o = 16; o > 0; o >>= 1) unsat |= __shfl_xor_sync(0xffffffffu, unsat, o);
         if ((threadIdx.x & 31) == 0 && unsat) atomicOr(a.unsat + (t & 1), unsat);
         grid.sync();
-        const uint32_t u = *((volatile uint32_t *)a.unsat + (t & 1));
-        const uint32_t newly = all & ~done & ~u;  // zero syndrome at round t
+        const Mask u = *((volatile Mask *)a.unsat + (t & 1));
+        const Mask newly = all & ~done & ~u;  // zero syndrome at round t
         if (tid < a.B && ((newly >> tid) & 1u) && a.early) {
             a.succ[tid] = 1;
             a.iters[tid] = t;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(kGridThreads) k_grid(const __grid_constant__ G
     }
     // codewords still running: ran out of rounds (early stop) or fixed iterations
     if (tid < a.B && !((done >> tid) & 1u)) {
-        const uint32_t u = *((volatile uint32_t *)a.unsat + (t & 1));
+        const Mask u = *((volatile Mask *)a.unsat + (t & 1));
         a.succ[tid] = ((u >> tid) & 1u) ? 0 : 1;
         a.iters[tid] = a.max_iter;
     }
@@ -150,7 +151,7 @@ int g_grid_blocks[64] = {};  // resident blocks per SM, per device
 }  // namespace
 
 size_t grid_workspace_bytes(const ldpc_graph *g, int32_t B) {
-    return (size_t)B * ((size_t)g->E * 8 + (size_t)g->n * 8 + (size_t)g->n) + 64;
+    return (size_t)B * ((size_t)g->E * 8 + (size_t)g->n * 8 + (size_t)g->n) + 256;
 }
 
 bool grid_suitable(const ldpc_graph *g, int32_t B) {
@@ -192,7 +193,7 @@ int launch_grid(const ldpc_graph *g, const double *in, const double *sig2, int32
     auto *base = static_cast<unsigned char *>(ws);
     a.msg = reinterpret_cast<double *>(base);
     a.pr = a.msg + (size_t)B * g->E;
-    a.unsat = reinterpret_cast<uint32_t *>(a.pr + (size_t)B * g->n);
+    a.unsat = reinterpret_cast<unsigned long long *>(a.pr + (size_t)B * g->n);
     a.chat = reinterpret_cast<uint8_t *>(a.unsat + 16);
     a.est = est;
     a.succ = succ;

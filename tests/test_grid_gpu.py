@@ -25,7 +25,8 @@ def _same(a, b):
 
 @pytest.mark.parametrize("code,B,ebno,iters", [("C3", 1, 2.0, 50), ("C3", 5, 1.0, 12), ("C2", 8, 1.5, 30),
                                                ("C1", 3, 1.0, 0), ("C1", 7, 0.5, 25), ("C2", 32, 1.25, 20),
-                                               ("C3", 13, 2.0, 15)])
+                                               ("C3", 13, 2.0, 15), ("C2", 33, 1.5, 20), ("C2", 64, 1.25, 20),
+                                               ("C1", 50, 1.0, 30)])
 @pytest.mark.parametrize("early", [True, False])
 def test_grid_equals_stream_and_oracle(cuda, code, B, ebno, iters, early):
     from oracle import OracleTables
@@ -65,7 +66,7 @@ def test_grid_refusals(cuda):
             dec.decode_priors(P, 5, schedule="grid")
         dec.decode_priors(P, 5)  # auto: streams
     H1 = configs.code("C1")
-    _, _, P1 = _frames(H1, 33, 1.0, 2)
-    with ParallelDecoder(CodeTables.from_matrix(H1), max_batch=33) as dec:
+    _, _, P1 = _frames(H1, 65, 1.0, 2)
+    with ParallelDecoder(CodeTables.from_matrix(H1), max_batch=65) as dec:
         with pytest.raises(ValueError):
-            dec.decode_priors(P1, 5, schedule="grid")  # more than 32 codewords
+            dec.decode_priors(P1, 5, schedule="grid")  # more than 64 codewords

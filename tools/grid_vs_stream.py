@@ -12,9 +12,9 @@ for name, it in (("C3", 50), ("C2", 50)):
     H = configs.code(name)
     s2 = configs.sigma2_for(name, 2.0)
     rng = np.random.default_rng(3)
-    P = torch.from_numpy(priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((32, H.n)), s2)).cuda()
+    P = torch.from_numpy(priors_awgn_batch(-1.0 + np.sqrt(s2) * rng.standard_normal((64, H.n)), s2)).cuda()
     with ParallelDecoder(CodeTables.from_matrix(H), max_batch=64) as dec:
-        for B in (1, 4, 8, 16, 32):
+        for B in (1, 4, 8, 16, 32, 48, 64):
             Pb = P[:B].contiguous()
             ws, outs = dec.workspace(B), dec.alloc_outputs(B, P.device)
             row = []
