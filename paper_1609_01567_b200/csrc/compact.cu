@@ -10,15 +10,20 @@
 //     (bit-sliced chat -> the caller's packed rows, through the position ->
 //     codeword map), success = 1, iterations, an all-zero syndrome row;
 //   * moves the live codewords' state (messages and priors, the only state
-//     that crosses a round) to positions 0..L-1 in codeword order, in place:
-//     one warp per row walks the output chunks in ascending order, so every
-//     source position it still has to read lies above everything it wrote;
+//     that crosses a round) into positions 0..L-1, in place.  Default (fill):
+//     the live codewords at positions >= L move into the stopped positions
+//     below L, i-th source into i-th hole -- only those move, and sources and
+//     destinations are disjoint.  LDPC_COMPACT_MODE=stable: all live codewords
+//     shift down in order; one warp per row walks the output chunks upward, so
+//     every source it still has to read lies above everything it wrote;
 //   * rewrites the maps and done masks (positions >= L become padding, done).
 // Codewords are independent and each keeps its own arithmetic, so results are
 // bit-identical to the uncompacted decode.  Everything stays on the device
 // (the decision is data dependent, so every kernel is launched every round and
 // the row move / retire exit at once when the plan says "no").
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -34,9 +39,9 @@ constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads) k_compact_plan(uint32_t *done, uint32_t *unsat, int32_t *iters,
                                                                int32_t NW, int32_t round, int32_t *orig,
                                                                int32_t *ret_orig, int32_t *perm, uint32_t *ret_sel,
-                                                               int32_t *ctl, int frac_pct) {
-    __shared__ int scan[kPlanThreads];
-    __shared__ int first_moved;
+                                                               int32_t *ctl, int frac_pct, int fill) {
+    __shared__ int warp_tot[kPlanThreads / 32];
+    __shared__ int first_moved, live_below_L;
     const int t = threadIdx.x;
     for (int w = t; w < NW; w += kPlanThreads) {
         const uint32_t d = done[w], newly = ~d & ~unsat[w];
@@ -51,17 +56,25 @@ __global__ void __launch_bounds__(kPlanThreads) k_compact_plan(uint32_t *done, u
     const int w0 = min(NWa, t * per), w1 = min(NWa, w0 + per);
     int live = 0;
     for (int w = w0; w < w1; w++) live += __popc(~done[w]);
-    scan[t] = live;
+    // exclusive scan of the live counts: shuffles within warps, then over the 32 warp totals
+    const int lane = t & 31;
+    int incl = live;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    if (lane == 31) warp_tot[t >> 5] = incl;
     if (t == 0) first_moved = INT32_MAX;
     __syncthreads();
-    for (int o = 1; o < kPlanThreads; o <<= 1) {  // inclusive Hillis-Steele scan
-        const int x = t >= o ? scan[t - o] : 0;
-        __syncthreads();
-        scan[t] += x;
-        __syncthreads();
+    int wt = lane < kPlanThreads / 32 ? warp_tot[lane] : 0, wincl = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, wincl, o);
+        if (lane >= o) wincl += x;
     }
-    const int L = scan[kPlanThreads - 1];
-    const int base = scan[t] - live;
+    const int L = __shfl_sync(0xffffffffu, wincl, 31);
+    const int base = __shfl_sync(0xffffffffu, wincl - wt, t >> 5) + incl - live;
     const int new_act = (L + 63) / 64;
     const bool go = new_act < act && (int64_t)new_act * 100 <= (int64_t)act * frac_pct;
     __syncthreads();  // every thread has read ctl[0] and the scan before ctl changes
@@ -70,22 +83,54 @@ __global__ void __launch_bounds__(kPlanThreads) k_compact_plan(uint32_t *done, u
         return;
     }
     if (t == 0) ctl[4] = act;
-    // pass 1: the live positions in order, the old map (for retiring), the old done words
-    int k = base;
-    for (int w = w0; w < w1; w++) {
-        const uint32_t d = done[w];
-        ret_sel[w] = d;
-        for (uint32_t x = ~d; x; x &= x - 1) {
-            const int p = 32 * w + __ffs(x) - 1;
-            perm[k] = p;
-            if (p != k) atomicMin(&first_moved, k);
-            k++;
+    if (fill) {
+        // hole filling: the live codewords at positions >= L move into the stopped positions below L,
+        // the i-th such source into the i-th hole (perm[i] = hole, perm[half + i] = source)
+        if (32 * w0 <= L && L < 32 * w1) {
+            int c = base;
+            for (int w = w0; 32 * (w + 1) <= L; w++) c += __popc(~done[w]);
+            if (L & 31) c += __popc(~done[L >> 5] & ((1u << (L & 31)) - 1u));
+            live_below_L = c;
         }
+        if (t == 0 && L >= 32 * NWa) live_below_L = L;
+        __syncthreads();
+        const int K = L - live_below_L, half = 16 * NW, src0 = L - K;
+        int k = base;
+        for (int w = w0; w < w1; w++) {
+            const uint32_t d = done[w];
+            ret_sel[w] = d;
+            for (int b = 0; b < 32; b++) {
+                const int p = 32 * w + b;
+                const bool lv = !((d >> b) & 1u);
+                if (p < L && !lv) perm[p - k] = p;
+                if (p >= L && lv) perm[half + k - src0] = p;
+                k += lv;
+            }
+        }
+        for (int p = t; p < 64 * act; p += kPlanThreads) ret_orig[p] = orig[p];
+        __syncthreads();
+        for (int p = L + t; p < 64 * act; p += kPlanThreads) orig[p] = -1;
+        for (int i = t; i < K; i += kPlanThreads) orig[perm[i]] = ret_orig[perm[half + i]];
+        if (t == 0) ctl[3] = K;
+    } else {
+        // stable: the live positions in order (perm[new] = old), everything from the first change moves
+        int k = base;
+        for (int w = w0; w < w1; w++) {
+            const uint32_t d = done[w];
+            ret_sel[w] = d;
+            for (uint32_t x = ~d; x; x &= x - 1) {
+                const int p = 32 * w + __ffs(x) - 1;
+                perm[k] = p;
+                if (p != k) atomicMin(&first_moved, k);
+                k++;
+            }
+        }
+        for (int p = t; p < 64 * act; p += kPlanThreads) ret_orig[p] = orig[p];
+        __syncthreads();
+        for (int p = t; p < 64 * act; p += kPlanThreads) orig[p] = p < L ? ret_orig[perm[p]] : -1;
+        if (t == 0) ctl[3] = first_moved == INT32_MAX ? new_act : first_moved / 64;
     }
-    for (int p = t; p < 64 * act; p += kPlanThreads) ret_orig[p] = orig[p];
-    __syncthreads();
-    // pass 2: the new map and done words (positions >= L: padding, stopped)
-    for (int p = t; p < 64 * act; p += kPlanThreads) orig[p] = p < L ? ret_orig[perm[p]] : -1;
+    // the new done words (positions >= L: padding, stopped)
     for (int w = t; w < NWa; w += kPlanThreads) {
         const int lo = 32 * w;
         done[w] = lo >= L ? 0xffffffffu : (L - lo >= 32 ? 0u : ~((1u << (L - lo)) - 1u));
@@ -94,7 +139,6 @@ __global__ void __launch_bounds__(kPlanThreads) k_compact_plan(uint32_t *done, u
         ctl[0] = new_act;
         ctl[1] = 1;
         ctl[2] = L;
-        ctl[3] = first_moved == INT32_MAX ? new_act : first_moved / 64;
     }
 }
 
@@ -135,6 +179,27 @@ __device__ __forceinline__ void move_row(T *a, int32_t rows, int32_t r, const in
     }
 }
 
+// Hole filling of one row: position perm[i] (< L, stopped) takes position perm[half + i] (>= L, live).
+// Sources and destinations are disjoint, so no ordering is needed.
+template <typename T>
+__device__ __forceinline__ void move_fill(T *a, int32_t rows, int32_t r, const int32_t *__restrict__ perm, int half,
+                                          int K, int lane) {
+    constexpr int U = 4;
+    for (int i0 = 0; i0 < K; i0 += 32 * U) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = i0 + 32 * u + lane;
+            if (i < K) v[u] = a[cofs(rows, r, __ldg(perm + half + i))];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = i0 + 32 * u + lane;
+            if (i < K) a[cofs(rows, r, __ldg(perm + i))] = v[u];
+        }
+    }
+}
+
 // Everything a compaction point does after its plan, in one launch (exits at once when the plan
 // said "no"): warps over
 //   [0, T0)        retire estimate bits, one (row block, word) tile each: a 32x32 ballot transpose
@@ -145,11 +210,11 @@ __global__ void k_compact_apply(const uint32_t *__restrict__ chat, int32_t n, in
                                 const uint32_t *__restrict__ ret_sel, const int32_t *__restrict__ ret_orig,
                                 const int32_t *__restrict__ iters_ws, const int32_t *__restrict__ ctl, DecodeOut out,
                                 int32_t RWm, int32_t B, const int32_t *__restrict__ perm, MoveArrays arr,
-                                int retire) {
+                                int retire, int fill, int half) {
     if (ctl[1] == 0) return;
     const int lane = threadIdx.x & 31;
     const int NWa = 2 * ctl[4];  // the words active before the plan: ret_sel / ret_orig cover exactly those
-    const int L = ctl[2], oc0 = ctl[3], new_act = ctl[0];
+    const int L = ctl[2], oc0 = ctl[3], new_act = ctl[0];  // oc0: first moved chunk, or the hole count (fill)
     const int RWn = (n + 31) / 32;
     const int64_t T0 = retire ? (int64_t)RWn * NWa : 0, T1 = retire ? NWa : 0;
     int64_t total = T0 + T1;
@@ -185,10 +250,16 @@ __global__ void k_compact_apply(const uint32_t *__restrict__ chat, int32_t n, in
             int64_t r = g - T0 - T1;
             int i = 0;
             while (r >= arr.rows[i]) r -= arr.rows[i++];
-            if (arr.elem[i] == 8)
+            if (fill) {  // oc0 = the number of holes filled
+                if (arr.elem[i] == 8)
+                    move_fill(static_cast<double *>(arr.p[i]), arr.rows[i], (int32_t)r, perm, half, oc0, lane);
+                else
+                    move_fill(static_cast<float *>(arr.p[i]), arr.rows[i], (int32_t)r, perm, half, oc0, lane);
+            } else if (arr.elem[i] == 8) {
                 move_row(static_cast<double *>(arr.p[i]), arr.rows[i], (int32_t)r, perm, L, oc0, new_act, lane);
-            else
+            } else {
                 move_row(static_cast<float *>(arr.p[i]), arr.rows[i], (int32_t)r, perm, L, oc0, new_act, lane);
+            }
         }
     }
 }
@@ -241,6 +312,30 @@ unsigned blocks_of(int64_t work, int threads, int64_t cap = 148 * 16) {
     return (unsigned)std::max<int64_t>(1, std::min(b, cap));
 }
 
+// k_compact_apply runs every round and exits at once on most of them, where each block of its grid
+// costs dispatch time: one resident wave (SMs x blocks per SM) and a grid-stride loop.
+int64_t apply_wave() {
+    static const int64_t wave = [] {
+        int dev = 0, sms = 148, per = 4;
+        if (cudaGetDevice(&dev) == cudaSuccess) {
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_compact_apply, 256, 0);
+        }
+        cudaGetLastError();
+        return (int64_t)std::max(sms, 1) * std::max(per, 1);
+    }();
+    return wave;
+}
+
+// LDPC_COMPACT_MODE=fill|stable: how the live codewords move (default fill)
+int compact_fill() {
+    static const int v = [] {
+        const char *e = getenv("LDPC_COMPACT_MODE");
+        return (e && std::string(e) == "stable") ? 0 : 1;
+    }();
+    return v;
+}
+
 }  // namespace
 
 int launch_compact_init(const Workspace &w, cudaStream_t s) {
@@ -257,8 +352,9 @@ int launch_compact(const ldpc_graph *g, const Workspace &w, int32_t round, int f
                    const CompactArray *arrays, int count, cudaStream_t s, cudaStream_t side,
                    cudaEvent_t fork) {
     LDPC_ARG_CHECK(count >= 1 && count <= 3, "compaction moves 1..3 arrays");
+    const int fill = compact_fill();
     k_compact_plan<<<1, kPlanThreads, 0, s>>>(w.done, w.unsat, w.iters, w.NW, round, w.orig, w.ret_orig, w.perm,
-                                              w.ret_sel, w.ctl, frac_pct);
+                                              w.ret_sel, w.ctl, frac_pct, fill);
     LDPC_CHECK_LAUNCH();
     MoveArrays first{}, rest{};
     first.p[0] = arrays[0].p;
@@ -280,11 +376,11 @@ int launch_compact(const ldpc_graph *g, const Workspace &w, int32_t round, int f
         s2 = side;
     }
     const int64_t tiles = (int64_t)((g->n + 31) / 32) * w.NW;
-    k_compact_apply<<<blocks_of(32 * std::max<int64_t>(rows_rest, tiles), 256, 148 * 32), 256, 0, s2>>>(
-        w.chat, g->n, w.NWs, w.ret_sel, w.ret_orig, w.iters, w.ctl, out, (g->m + 31) / 32, w.B, w.perm, rest, 1);
+    k_compact_apply<<<blocks_of(32 * std::max<int64_t>(rows_rest, tiles), 256, apply_wave()), 256, 0, s2>>>(
+        w.chat, g->n, w.NWs, w.ret_sel, w.ret_orig, w.iters, w.ctl, out, (g->m + 31) / 32, w.B, w.perm, rest, 1, fill, 16 * w.NW);
     LDPC_CHECK_LAUNCH();
-    k_compact_apply<<<blocks_of(32 * (int64_t)arrays[0].rows, 256, 148 * 32), 256, 0, s>>>(
-        w.chat, g->n, w.NWs, w.ret_sel, w.ret_orig, w.iters, w.ctl, out, (g->m + 31) / 32, w.B, w.perm, first, 0);
+    k_compact_apply<<<blocks_of(32 * (int64_t)arrays[0].rows, 256, apply_wave()), 256, 0, s>>>(
+        w.chat, g->n, w.NWs, w.ret_sel, w.ret_orig, w.iters, w.ctl, out, (g->m + 31) / 32, w.B, w.perm, first, 0, fill, 16 * w.NW);
     LDPC_CHECK_LAUNCH();
     return LDPC_OK;
 }

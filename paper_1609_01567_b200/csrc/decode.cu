@@ -502,7 +502,7 @@ static CompactFork *compact_fork(cudaStream_t s) {
 static int compact_pct() {
     static const int v = [] {
         const char *e = getenv("LDPC_COMPACT");
-        return e ? std::max(0, std::min(100, atoi(e))) : 75;
+        return e ? std::max(0, std::min(100, atoi(e))) : 80;
     }();
     return v;
 }

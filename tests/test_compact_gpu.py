@@ -1,7 +1,8 @@
 """Per-codeword early stop (serial.py:169-177, engine.py:341-347): live codewords are compacted
 into dense chunks on the device (compact.cu) so the work follows each codeword's stopping round.
 Results must be bit-identical to the oracle and to the uncompacted decode, whatever the
-compaction points are (LDPC_COMPACT=<pct> threshold, 0 = off; read once per process)."""
+compaction points are (LDPC_COMPACT=<pct> threshold, 0 = off; LDPC_COMPACT_MODE=fill|stable; read once per
+process)."""
 
 from __future__ import annotations
 
@@ -71,8 +72,9 @@ np.savez({path!r}, **out)
 
 
 def _run(tmp_path, env_value, code, B, ebno, iters):
-    path = str(tmp_path / f"out_{env_value}.npz")
-    env = dict(os.environ, LDPC_COMPACT=env_value)
+    pct, _, mode = env_value.partition(":")
+    path = str(tmp_path / f"out_{pct}_{mode}.npz")
+    env = dict(os.environ, LDPC_COMPACT=pct, LDPC_COMPACT_MODE=mode or "fill")
     src = _RUN.format(root=str(ROOT), code=code, B=B, ebno=ebno, iters=iters, path=path)
     r = subprocess.run([sys.executable, "-c", src], capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
@@ -81,11 +83,13 @@ def _run(tmp_path, env_value, code, B, ebno, iters):
 
 @pytest.mark.parametrize("code,B,ebno,iters", [("C2", 448, 2.0, 20), ("C4", 192, 3.0, 20)])
 def test_compaction_points_do_not_change_results(cuda, tmp_path, code, B, ebno, iters):
-    # off, the default threshold, and compaction at every round that frees a chunk
-    runs = {v: _run(tmp_path, v, code, B, ebno, iters) for v in ("0", "75", "100")}
+    # off, the default threshold, and compaction at every round that frees a chunk; live codewords
+    # moved into the stopped positions (fill, default) or shifted down in order (stable)
+    modes = ("75", "80", "100", "80:stable", "100:stable")
+    runs = {v: _run(tmp_path, v, code, B, ebno, iters) for v in ("0",) + modes}
     base = runs["0"]
     assert len(set(base["fp64_it"].tolist())) > 3
-    for v in ("75", "100"):
+    for v in modes:
         for k in base.files:
             assert np.array_equal(runs[v][k], base[k]), (v, k)
 
