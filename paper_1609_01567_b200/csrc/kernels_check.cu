@@ -318,7 +318,9 @@ int launch_chains(const NodeLaunch &a, int max_deg, size_t smem, bool from_prior
     const bool r16 = r_env ? r_env == 16 : (max_deg + 15) / 16 >= 48;
     auto kern = from_prior ? k_check_chains<TW, true, GS> : k_check_chains<TW, false, GS>;
     if (r16) kern = from_prior ? k_check_chains<TW, true, GS, 16> : k_check_chains<TW, false, GS, 16>;
-    if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the cap (not this launch's size): launches of one instantiation with different tiles may be issued
+    // from several threads or side streams
+    if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmemBudget));
     const int64_t blocks = (int64_t)a.node_count * (a.Bp / TW);
     kern<<<(unsigned)blocks, 32 * chain_warps(max_deg, r16 ? 16 : kWideR), smem, s>>>(a, max_deg);
     LDPC_CHECK_LAUNCH();

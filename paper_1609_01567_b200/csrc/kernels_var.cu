@@ -328,7 +328,9 @@ __global__ void __launch_bounds__(kChainThreads) k_var_chains(NodeLaunch a, int 
 template <int TW, bool GS>
 int launch_var_chains(const NodeLaunch &a, int max_deg, size_t smem, bool write_q, cudaStream_t s) {
     auto kern = write_q ? k_var_chains<TW, true, GS> : k_var_chains<TW, false, GS>;
-    if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the cap (not this launch's size): launches of one instantiation with different tiles may be issued
+    // from several threads or side streams
+    if (smem) LDPC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmemBudget));
     const int64_t blocks = (int64_t)a.node_count * (a.Bp / TW);
     // warps: two groups each (balanced band pairs), up to 32
     const int nw = std::max(1, std::min(32, ((max_deg + kChainR - 1) / kChainR + 1) / 2));
