@@ -378,3 +378,21 @@ def test_matrix_keyed_device_tables_are_released(cuda):
     gc.collect()
     assert not dict.__contains__(D._H_TABLES, key)
     assert graph() is None
+
+
+@pytest.mark.parametrize("code,B,schedules", [("C1", 40, ("stream", "onchip")), ("C2", 64, ("stream", "grid")),
+                                               ("C4", 6, ("stream",))])
+def test_high_snr_fixed_iterations_vs_oracle(cuda, code, B, schedules):
+    """5 dB, fixed 12 rounds: the messages saturate (variable-side numerators of exactly 0 over
+    positive denominators) for most of the decode; every schedule gives the oracle's outputs."""
+    from oracle import OracleTables
+
+    H, P = _frames(code, B, 5.0, seed=5 + B)
+    est_o, ok_o, it_o, z_o = OracleTables.from_matrix(H).decode_batch(P, 12, fixed_iterations=True)
+    with ParallelDecoder(CodeTables.from_matrix(H), max_batch=B) as dec:
+        for schedule in schedules:
+            res = dec.decode_priors(P, 12, early_stop=False, schedule=schedule)
+            assert np.array_equal(res.estimates(), est_o), schedule
+            assert np.array_equal(res.success.astype(bool), ok_o), schedule
+            assert np.array_equal(res.iterations, it_o), schedule
+            assert np.array_equal(res.syndromes(), z_o), schedule

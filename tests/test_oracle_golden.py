@@ -49,6 +49,22 @@ def test_phases_match_reference(golden_tables, golden_phases):
             assert np.array_equal(T.syndrome(g("chat_in")[i]), g("syndrome")[i]), name
 
 
+def test_saturated_phases_match_reference(golden_saturated):
+    """High-SNR states (0 / 1 / -0.0 / denormal priors and messages; tests/golden/make_saturated_golden.py):
+    the oracle's zero numerators, zero denominators and signed zeros are the reference's bits."""
+    g = golden_saturated
+    for name in g["names"]:
+        n, m = g[f"{name}/nm"]
+        T = OracleTables(n, m, g[f"{name}/ones"])
+        for i in range(g[f"{name}/p"].shape[0]):
+            q = T.values_to_check(g[f"{name}/p"][i], g[f"{name}/r"][i])
+            assert np.array_equal(q.view(np.uint64), g[f"{name}/to_check"][i].view(np.uint64)), name
+            r = T.values_to_variable(g[f"{name}/q"][i])
+            assert np.array_equal(r.view(np.uint64), g[f"{name}/to_variable"][i].view(np.uint64)), name
+            assert np.array_equal(T.estimate(g[f"{name}/p"][i], g[f"{name}/r"][i]), g[f"{name}/estimate"][i]), name
+        assert np.signbit(g[f"{name}/to_check"]).any()  # the fixture does hold -0.0 outputs
+
+
 def test_decode_matches_reference(golden_tables, golden_decode):
     for key in golden_decode["cases"]:
         code = str(golden_decode[f"{key}/code"])

@@ -72,6 +72,48 @@ def test_random_states_vs_oracle(cuda, code, B):
         assert np.array_equal(z[b], O.syndrome(C[b])), (code, b)
 
 
+def test_saturated_golden(cuda, golden_saturated):
+    """The reference's outputs on high-SNR states (tests/golden/saturated.npz), all states batched."""
+    g = golden_saturated
+    for name in g["names"]:
+        n, m = (int(x) for x in g[f"{name}/nm"])
+        T = CodeTables.from_matrix(ParityCheckMatrix(n, m, g[f"{name}/ones"]))
+        k = lambda key: g[f"{name}/{key}"]  # noqa: E731
+        assert np.array_equal(bits(values_to_check(k("p"), k("r"), T)), bits(k("to_check"))), name
+        assert np.array_equal(bits(values_to_variable(k("q"), T)), bits(k("to_variable"))), name
+        assert np.array_equal(estimate(k("p"), k("r"), T), k("estimate")), name
+
+
+@pytest.mark.parametrize("code,B", [("C1", 4), ("C2", 3), ("C4", 2)])
+def test_saturated_states_vs_oracle(cuda, code, B):
+    """High-SNR states: messages and priors at exactly 0 / 1 (and -0.0, denormals, tiny values),
+    so most variable-side numerators q1 are +-0 over a positive denominator, some denominators are
+    0 (the reference's 1/2) and some tiny.  Every slow-path division branch of every variable kernel
+    family (ring, register, mid-degree, chains at C4) must give the oracle's bits, signs included."""
+    from oracle import OracleTables
+
+    H = configs.code(code)
+    T = CodeTables.from_matrix(H)
+    O = OracleTables.from_matrix(H)
+    rng = np.random.default_rng(7 + sum(map(ord, code)))
+    special = np.array([0.0, -0.0, 1.0, 5e-324, 1e-300, 1e-160, 1.0 - 2.0 ** -53, 0.5])
+
+    def draw(shape, frac):
+        x = rng.uniform(size=shape)
+        pick = rng.uniform(size=shape) < frac
+        x[pick] = special[rng.integers(0, special.size, size=int(pick.sum()))]
+        return x
+
+    P = draw((B, H.n), 0.5)
+    R = draw((B, H.total_edges), 0.6)
+    R[:, : H.total_edges // 3] = rng.choice([0.0, 1.0], size=(B, H.total_edges // 3))
+    q = values_to_check(P, R, T)
+    c = estimate(P, R, T)
+    for b in range(B):
+        assert np.array_equal(bits(q[b]), bits(O.values_to_check(P[b], R[b]))), (code, b)
+        assert np.array_equal(c[b], O.estimate(P[b], R[b])), (code, b)
+
+
 # ---- test_serial.py KATs, run on the GPU kernels ----------------------------
 
 class TestValuesToCheck:
